@@ -1,0 +1,302 @@
+/*
+ * capsim_oracle.c — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+ *
+ * A plain-C, scalar restatement of the reference's trace-driven policy-evaluation hot
+ * path (capsim 0.1.0, /root/reference/pkg/src/capsim). Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.
+ *
+ * Pinned against the reference itself: the JSON fixtures under tests/golden were produced by importing the
+ * reference package in the build container (tests/golden/make_golden.py) and
+ * tests/test_oracle_golden.py checks every vector against this file.
+ *
+ * Every function names the reference lines it restates:
+ *   ora_regime_member   policy.py:100-107   (_regime_entries)
+ *   ora_prefer          policy.py:90-97     (_prefer: higher ips, then lower (power, mtl, bs))
+ *   ora_index_build     policy.py:118-134   (PolicyIndex.__init__: sort by (power,mtl,bs) + prefix best)
+ *   ora_index_select    policy.py:136-148   (PolicyIndex.select: bisect_right, idle when 0)
+ *   ora_bruteforce      tests/conftest.py:100-129 (independent linear-scan argmax)
+ *   ora_fsum            CPython math.fsum   (exactly rounded sum; used by sim.py:126-127)
+ *   ora_aggregate       sim.py:104-127      (_aggregate: switch penalty, energy proxy, idle count)
+ *   ora_simulate        sim.py:130-188      (simulate: per-step selection + aggregate)
+ *   ora_simulate_batch  loops ora_simulate over (trace, grid, policy) with pthreads — the
+ *                       CPU baseline ("port") the bench times beside the GPU.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORA_BATCHING 0
+#define ORA_MULTI_TENANT 1
+#define ORA_COMBINATION 2
+
+typedef struct {
+  int32_t mtl, bs;
+  double thr, pw;
+  int32_t idx; /* position in the caller's entry arrays */
+} ora_entry;
+
+/* policy.py:100-107 */
+static int ora_regime_member(int regime, int32_t mtl, int32_t bs, int batching_mtl, int mt_bs) {
+  if (regime == ORA_BATCHING) return mtl == batching_mtl;
+  if (regime == ORA_MULTI_TENANT) return bs == mt_bs;
+  return 1;
+}
+
+/* lexicographic (power, mtl, bs) comparison used by both the sort key (policy.py:129)
+ * and the tie-break of _prefer (policy.py:95-97). */
+static int ora_key_cmp(const ora_entry* a, const ora_entry* b) {
+  if (a->pw < b->pw) return -1;
+  if (a->pw > b->pw) return 1;
+  if (a->mtl != b->mtl) return a->mtl < b->mtl ? -1 : 1;
+  if (a->bs != b->bs) return a->bs < b->bs ? -1 : 1;
+  return 0;
+}
+
+static int ora_qsort_cmp(const void* a, const void* b) {
+  return ora_key_cmp((const ora_entry*)a, (const ora_entry*)b);
+}
+
+/* policy.py:90-97: returns 1 when a is preferred over b */
+static int ora_prefer_a(const ora_entry* a, const ora_entry* b) {
+  if (a->thr != b->thr) return a->thr > b->thr;
+  return ora_key_cmp(a, b) <= 0;
+}
+
+/*
+ * policy.py:118-134. Fills, for the regime's entries sorted by (power, mtl, bs):
+ *   powers[i]   = power of the i-th sorted entry
+ *   best_idx[i] = caller index of the prefix-best entry among sorted[0..i]
+ * Returns the regime size n_reg (<= n).
+ */
+int ora_index_build(const int32_t* mtl, const int32_t* bs, const double* thr, const double* pw, int n,
+                    int regime, int batching_mtl, int mt_bs, double* powers, int32_t* best_idx) {
+  ora_entry* e = (ora_entry*)malloc(sizeof(ora_entry) * (size_t)(n > 0 ? n : 1));
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!ora_regime_member(regime, mtl[i], bs[i], batching_mtl, mt_bs)) continue;
+    e[m].mtl = mtl[i]; e[m].bs = bs[i]; e[m].thr = thr[i]; e[m].pw = pw[i]; e[m].idx = i;
+    ++m;
+  }
+  /* (mtl, bs) are unique in a grid, so the key is a strict total order and an unstable
+   * sort gives the same result as Python's stable sort. */
+  qsort(e, (size_t)m, sizeof(ora_entry), ora_qsort_cmp);
+  int best = -1;
+  for (int i = 0; i < m; ++i) {
+    powers[i] = e[i].pw;
+    if (best < 0 || !ora_prefer_a(&e[best], &e[i])) best = i;
+    best_idx[i] = e[best].idx;
+  }
+  free(e);
+  return m;
+}
+
+/* policy.py:136-148 (caller has already rejected cap < 0). Returns feasible_count;
+ * *sel = caller index of the selection or -1 for IDLE_SELECTION. */
+int64_t ora_index_select(const double* powers, const int32_t* best_idx, int n_reg, double cap, int32_t* sel) {
+  /* bisect.bisect_right: first position whose power is > cap */
+  int lo = 0, hi = n_reg;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (cap < powers[mid]) hi = mid; else lo = mid + 1;
+  }
+  *sel = lo == 0 ? -1 : best_idx[lo - 1];
+  return lo;
+}
+
+/* tests/conftest.py:100-129: independent brute-force argmax (no shared code with the index). */
+int32_t ora_bruteforce(const int32_t* mtl, const int32_t* bs, const double* thr, const double* pw, int n,
+                       int regime, int batching_mtl, int mt_bs, double cap) {
+  int32_t best = -1;
+  for (int i = 0; i < n; ++i) {
+    if (pw[i] > cap) continue;
+    if (!ora_regime_member(regime, mtl[i], bs[i], batching_mtl, mt_bs)) continue;
+    if (best < 0) { best = i; continue; }
+    if (thr[i] > thr[best]) best = i;
+    else if (thr[i] == thr[best]) {
+      if (pw[i] < pw[best]) best = i;
+      else if (pw[i] == pw[best]) {
+        if (mtl[i] < mtl[best]) best = i;
+        else if (mtl[i] == mtl[best] && bs[i] < bs[best]) best = i;
+      }
+    }
+  }
+  return best;
+}
+
+/* CPython math.fsum (Shewchuk partials + half-even correction), finite inputs only. */
+typedef struct { double* p; int n, cap; } ora_partials;
+
+static void ora_partials_add(ora_partials* ps, double x) {
+  int i = 0;
+  for (int j = 0; j < ps->n; ++j) {
+    double y = ps->p[j];
+    if (fabs(x) < fabs(y)) { double t = x; x = y; y = t; }
+    double hi = x + y;
+    double lo = y - (hi - x);
+    if (lo != 0.0) ps->p[i++] = lo;
+    x = hi;
+  }
+  if (i >= ps->cap) {
+    ps->cap = ps->cap ? ps->cap * 2 : 32;
+    ps->p = (double*)realloc(ps->p, sizeof(double) * (size_t)ps->cap);
+  }
+  ps->p[i] = x;
+  ps->n = i + 1;
+}
+
+static double ora_partials_result(const ora_partials* ps) {
+  int n = ps->n;
+  double hi = 0.0;
+  if (n > 0) {
+    double lo = 0.0;
+    hi = ps->p[--n];
+    while (n > 0) {
+      double x = hi;
+      double y = ps->p[--n];
+      hi = x + y;
+      double yr = hi - x;
+      lo = y - yr;
+      if (lo != 0.0) break;
+    }
+    if (n > 0 && ((lo < 0.0 && ps->p[n - 1] < 0.0) || (lo > 0.0 && ps->p[n - 1] > 0.0))) {
+      double y = lo * 2.0;
+      double x = hi + y;
+      double yr = x - hi;
+      if (y == yr) hi = x;
+    }
+  }
+  return hi;
+}
+
+double ora_fsum(const double* x, int64_t n) {
+  ora_partials ps = {0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) ora_partials_add(&ps, x[i]);
+  double r = ora_partials_result(&ps);
+  free(ps.p);
+  return r;
+}
+
+/*
+ * sim.py:104-127 over per-step selections. sel[i] = caller entry index or -1 (idle).
+ * Outputs avg throughput, idle count and energy proxy exactly as the reference computes them.
+ */
+void ora_aggregate(const double* thr, const double* pw, const int32_t* sel, int64_t n_steps, int32_t step_seconds,
+                   double idle_power_w, double switch_penalty_s, double* avg, int64_t* idle, double* energy) {
+  double pen = switch_penalty_s < (double)step_seconds ? switch_penalty_s : (double)step_seconds;
+  double pf = pen / (double)step_seconds;
+  ora_partials pt = {0, 0, 0}, pe = {0, 0, 0};
+  int64_t idle_count = 0;
+  int32_t prev = -1;
+  for (int64_t i = 0; i < n_steps; ++i) {
+    int32_t s = sel[i];
+    double ips = s < 0 ? 0.0 : thr[s];
+    if (i > 0 && pf > 0.0 && s != prev) ips *= 1.0 - pf;
+    ora_partials_add(&pt, ips);
+    double p = s < 0 ? idle_power_w : pw[s];
+    ora_partials_add(&pe, p * (double)step_seconds / 3600.0);
+    if (s < 0) ++idle_count;
+    prev = s;
+  }
+  *avg = ora_partials_result(&pt) / (double)n_steps;
+  *idle = idle_count;
+  *energy = ora_partials_result(&pe);
+  free(pt.p);
+  free(pe.p);
+}
+
+/*
+ * sim.py:130-188 for one (grid, trace, exhaustive policy). caps are fp64 (fp32 caps are
+ * widened exactly by the caller). step_sel / step_count (nullable) receive the per-step
+ * selection index and feasible_count. Returns 0, or -1 on a negative cap (policy.py:137).
+ */
+int ora_simulate(const int32_t* mtl, const int32_t* bs, const double* thr, const double* pw, int n,
+                 int regime, const double* caps, int64_t n_steps, int32_t step_seconds, double idle_power_w,
+                 double switch_penalty_s, int32_t* step_sel, int64_t* step_count, double* avg, int64_t* idle,
+                 double* energy) {
+  double* powers = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  int32_t* best = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  int32_t* sel = step_sel ? step_sel : (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_steps > 0 ? n_steps : 1));
+  int m = ora_index_build(mtl, bs, thr, pw, n, regime, 1, 1, powers, best);
+  int rc = 0;
+  for (int64_t i = 0; i < n_steps; ++i) {
+    if (caps[i] < 0.0) { rc = -1; break; }
+    int64_t c = ora_index_select(powers, best, m, caps[i], &sel[i]);
+    if (step_count) step_count[i] = c;
+  }
+  if (rc == 0) ora_aggregate(thr, pw, sel, n_steps, step_seconds, idle_power_w, switch_penalty_s, avg, idle, energy);
+  free(powers);
+  free(best);
+  if (!step_sel) free(sel);
+  return rc;
+}
+
+/* ---- batch driver: the CPU baseline timed by bench.py (reference algorithm, all host threads) ---- */
+
+typedef struct {
+  const int32_t* mtl; const int32_t* bs; const double* thr; const double* pw; int n;
+  double idle_power_w;
+} ora_grid;
+
+typedef struct {
+  const ora_grid* grids; int n_grids;
+  const float* caps; int64_t n_traces, n_steps;
+  int32_t step_seconds; double switch_penalty_s;
+  double* out_avg; int64_t* out_idle; double* out_energy; /* [trace][grid][policy] */
+  int64_t next; pthread_mutex_t mu;
+} ora_batch_job;
+
+static void* ora_batch_worker(void* arg) {
+  ora_batch_job* j = (ora_batch_job*)arg;
+  double* caps64 = (double*)malloc(sizeof(double) * (size_t)j->n_steps);
+  int32_t* sel = (int32_t*)malloc(sizeof(int32_t) * (size_t)j->n_steps);
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    int64_t t = j->next++;
+    pthread_mutex_unlock(&j->mu);
+    if (t >= j->n_traces) break;
+    const float* c = j->caps + t * j->n_steps;
+    for (int64_t i = 0; i < j->n_steps; ++i) caps64[i] = (double)c[i];
+    for (int g = 0; g < j->n_grids; ++g) {
+      const ora_grid* gr = &j->grids[g];
+      for (int p = 0; p < 3; ++p) {
+        int64_t o = (t * j->n_grids + g) * 3 + p;
+        ora_simulate(gr->mtl, gr->bs, gr->thr, gr->pw, gr->n, p, caps64, j->n_steps, j->step_seconds,
+                     gr->idle_power_w, j->switch_penalty_s, sel, NULL, &j->out_avg[o], &j->out_idle[o],
+                     &j->out_energy[o]);
+      }
+    }
+  }
+  free(caps64);
+  free(sel);
+  return NULL;
+}
+
+/* grids_* are flattened: entries of grid g live at [offs[g], offs[g+1]). Policy order in the
+ * output is (batching, multi-tenant, combination). Returns the thread count used. */
+int ora_simulate_batch(const int32_t* mtl, const int32_t* bs, const double* thr, const double* pw,
+                       const int64_t* offs, const double* idle_power_w, int n_grids, const float* caps,
+                       int64_t n_traces, int64_t n_steps, int32_t step_seconds, double switch_penalty_s,
+                       int n_threads, double* out_avg, int64_t* out_idle, double* out_energy) {
+  ora_grid* grids = (ora_grid*)malloc(sizeof(ora_grid) * (size_t)n_grids);
+  for (int g = 0; g < n_grids; ++g) {
+    grids[g].mtl = mtl + offs[g]; grids[g].bs = bs + offs[g];
+    grids[g].thr = thr + offs[g]; grids[g].pw = pw + offs[g];
+    grids[g].n = (int)(offs[g + 1] - offs[g]);
+    grids[g].idle_power_w = idle_power_w[g];
+  }
+  ora_batch_job j;
+  j.grids = grids; j.n_grids = n_grids; j.caps = caps; j.n_traces = n_traces; j.n_steps = n_steps;
+  j.step_seconds = step_seconds; j.switch_penalty_s = switch_penalty_s;
+  j.out_avg = out_avg; j.out_idle = out_idle; j.out_energy = out_energy; j.next = 0;
+  pthread_mutex_init(&j.mu, NULL);
+  if (n_threads < 1) n_threads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n_threads);
+  for (int i = 0; i < n_threads; ++i) pthread_create(&th[i], NULL, ora_batch_worker, &j);
+  for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+  pthread_mutex_destroy(&j.mu);
+  free(th);
+  free(grids);
+  return n_threads;
+}
