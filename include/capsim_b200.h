@@ -1,0 +1,165 @@
+/*
+ * capsim_b200.h — C ABI of the B200-native policy-evaluation engine (libcapsim_b200.so).
+ *
+ * The reference (capsim 0.1.0, pure Python) has no FFI: its boundary for this path is the
+ * Python API re-exported from pkg/src/capsim/__init__.py:8-116. Each entry point below names
+ * the reference function it replaces; paper_2306_12247_b200/_native.py is the ctypes
+ * binding and the package's policy.py / sim.py mirror the reference signatures on top of it.
+ *
+ * Conventions
+ *   - Every function returns int status: 0 = ok, < 0 = error (CS_E_*); the message of the
+ *     last error on the calling thread is cs_last_error().
+ *   - Plain pointers and sizes only. "dev" pointers are CUDA device pointers owned by the
+ *     caller (PyTorch tensors used as buffers); "host" pointers are host memory. No entry
+ *     point allocates device memory inside an evaluation call except cs_engine_* which owns
+ *     its pinned/device staging buffers for the host-buffer path.
+ *   - stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Policy index order everywhere: 0 = batching, 1 = multi-tenant, 2 = combination
+ *     (PolicyTag, policy.py:25-29).
+ */
+#ifndef CAPSIM_B200_H
+#define CAPSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_ABI_VERSION 1
+
+#define CS_OK 0
+#define CS_E_INVALID -1   /* bad argument (maps to ValueError / ValidationError) */
+#define CS_E_CUDA -2      /* CUDA runtime error */
+#define CS_E_NODEVICE -3  /* no usable sm_100 device */
+#define CS_E_UNSUPPORTED -4
+
+#define CS_CAP_F32 0 /* synthetic traces: fp32 caps, 4 B/timestep */
+#define CS_CAP_F64 1 /* drop-in PowerTrace values: fp64 caps, 8 B/timestep */
+
+#define CS_BATCHING 0
+#define CS_MULTI_TENANT 1
+#define CS_COMBINATION 2
+
+/* cs_eval flags */
+#define CS_FLAG_CHECK_VIOLATIONS 1u /* per-step power <= cap self-check (StepRecord, sim.py:50-54) */
+#define CS_FLAG_ACCUMULATE_HIST 2u  /* add into hist_out instead of overwriting it */
+
+/* One profiling grid (ProfileGrid, profile.py:57-106): n entries Config(mtl, bs) -> (ips, W). */
+typedef struct {
+  int32_t n_entries;
+  const int32_t* mtl;
+  const int32_t* bs;
+  const double* throughput_ips;
+  const double* power_w;
+  double idle_power_w; /* gpu_idle_power_w, or NaN when None (energy then uses 0 W, sim.py:175) */
+} cs_grid_desc;
+
+/* Per (trace, grid, policy) aggregate: SimReport's aggregates (sim.py:57-83, _aggregate sim.py:104-127). */
+typedef struct {
+  double avg_throughput_ips; /* fsum(ips)/num_steps, switch penalty applied (sim.py:119-126) */
+  double energy_proxy_wh;    /* fsum((power or idle) * step_seconds / 3600) (sim.py:122,127) */
+  int64_t idle_steps;        /* steps with no feasible config (sim.py:123-124) */
+  int64_t switches;          /* steps i>0 whose config differs from step i-1 (sim.py:119) */
+  int64_t violations;        /* steps whose selected power exceeds the cap: must be 0 (sim.py:50-54) */
+  int64_t num_steps;
+} cs_agg;
+
+typedef struct {
+  int32_t cap_dtype;
+  int32_t n_grids;
+  int32_t n_union_bins;    /* distinct thresholds over all grids + 1 */
+  int32_t max_grid_bins;
+  int32_t lut_entries;     /* level-1 + sub-tables */
+  int32_t lut_shift;
+  int32_t lut_level1;
+  int32_t lut_subtables;
+  int64_t device_bytes;    /* size of the staged device blob */
+} cs_tables_info;
+
+typedef struct cs_tables cs_tables;
+typedef struct cs_engine cs_engine;
+
+/* Evaluation of an exhaustive-policy sweep over a [n_traces x n_steps] cap matrix
+ * (simulate(), sim.py:130-188, for every (trace, grid, policy) at once). */
+typedef struct {
+  const void* caps;        /* dev, [n_traces][ld] fp32 or fp64 (cap_dtype of the tables), 16-B aligned */
+  int64_t n_traces;
+  int64_t n_steps;
+  int64_t ld;              /* row pitch in elements: multiple of 4 (fp32) / 2 (fp64), >= n_steps */
+  int32_t step_seconds;    /* PowerTrace.step_seconds (> 0) */
+  double switch_penalty_s; /* simulate(switch_penalty_s=...) (>= 0) */
+  uint32_t flags;          /* CS_FLAG_* */
+  uint16_t* step_bins;     /* dev, nullable: [n_traces][ld_bins] union bin per step (per-step mode) */
+  int64_t ld_bins;
+  cs_agg* agg;             /* dev, nullable: [n_traces][n_grids][3] */
+  uint64_t* hist;          /* dev, nullable: [n_union_bins] steps per union bin over all traces */
+  void* workspace;         /* dev, cs_eval_workspace_size() bytes (may be NULL when that is 0) */
+  size_t workspace_bytes;
+} cs_eval_args;
+
+/* ---- errors / version ---- */
+const char* cs_last_error(void);
+int cs_abi_version(void);
+/* Fills props: SM count, sm major/minor, smem per block; fails with CS_E_NODEVICE off-GPU. */
+int cs_device_query(int32_t device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---- N1 table staging: PolicyIndex.__init__ (policy.py:118-134) for all 3 regimes of all
+ *      grids at once, merged into one union-threshold rank table + bucketed LUT ---- */
+int cs_tables_create(const cs_grid_desc* grids, int32_t n_grids, int32_t cap_dtype, int32_t batching_mtl,
+                     int32_t multi_tenant_bs, cs_tables** out);
+int cs_tables_destroy(cs_tables* t);
+int cs_tables_get_info(const cs_tables* t, cs_tables_info* out);
+/* Host copies of the decoded selection per grid bin (the drop-in turns per-step bins into
+ * Selection records with these): sel = entry index in the caller's order or -1 (idle),
+ * count = feasible_count (policy.py:139-148). Arrays hold max_grid_bins elements. */
+int cs_tables_grid_bins(const cs_tables* t, int32_t grid, int32_t policy, int32_t* sel, int64_t* count,
+                        int32_t* n_bins);
+/* union bin -> grid bin map for one grid (n_union_bins uint16). */
+int cs_tables_union_map(const cs_tables* t, int32_t grid, uint16_t* out);
+/* Host restatement of the device bin lookup (for CPU tests of the staged LUT). */
+int cs_tables_lookup_host(const cs_tables* t, const void* caps, int64_t n, int32_t* bins_out);
+/* Upload the staged blob to a device (idempotent per device). */
+int cs_tables_upload(cs_tables* t, int32_t device);
+
+/* ---- N2+N3 per-timestep policy kernel + accumulation (simulate + _aggregate) ---- */
+int cs_eval_workspace_size(const cs_tables* t, const cs_eval_args* a, size_t* bytes);
+int cs_eval(const cs_tables* t, const cs_eval_args* a, void* stream);
+/* Device duration (ms) of the last cs_eval's main kernel launch on this thread, timed with
+ * CUDA events on the launching stream (valid after that stream is synchronized). */
+int cs_eval_last_kernel_ms(float* ms);
+/* Number of kernels the last cs_eval launched. */
+int cs_eval_last_launches(int32_t* n);
+
+/* ---- per-cap API: select_config (policy.py:172-188) and feasible_set (policy.py:151-169) as
+ *      warp-per-query argmax (shuffle) / ballot kernels over the grid's raw entries ---- */
+int cs_select_caps(const cs_tables* t, int32_t grid, int32_t policy, const double* caps_dev, int64_t n,
+                   int32_t* sel_dev, int64_t* count_dev, void* stream);
+/* words_per_cap = ceil(n_entries/32); bit j of word w set <=> entry 32w+j is feasible. */
+int cs_feasible_caps(const cs_tables* t, int32_t grid, int32_t policy, const double* caps_dev, int64_t n,
+                     uint32_t* mask_dev, void* stream);
+
+/* ---- host-buffer end-to-end path: pinned staging, H2D/compute/D2H overlapped on 2 streams ---- */
+int cs_engine_create(int32_t device, int64_t chunk_traces_max, int64_t n_steps_max, int32_t cap_dtype,
+                     cs_engine** out);
+int cs_engine_destroy(cs_engine* e);
+/* caps_host: [n_traces][ld] host memory; agg_host: [n_traces][n_grids][3]; hist_host:
+ * [n_union_bins] (nullable). Blocks until results are in host memory. */
+int cs_engine_eval_host(cs_engine* e, const cs_tables* t, const void* caps_host, int64_t n_traces, int64_t n_steps,
+                        int64_t ld, int32_t step_seconds, double switch_penalty_s, uint32_t flags, cs_agg* agg_host,
+                        uint64_t* hist_host, int64_t* h2d_bytes, int64_t* d2h_bytes);
+
+/* ---- synthetic traces for benchmarks (counter-based, keyed by (seed, global trace id)) ---- */
+#define CS_TRACE_SOLAR 0
+#define CS_TRACE_WIND 1
+#define CS_TRACE_MIXED 2   /* even global ids solar, odd wind */
+#define CS_TRACE_IID 3     /* iid uniform(0, peak) adversarial variant */
+int cs_generate_traces(float* caps_dev, int64_t n_traces, int64_t n_steps, int64_t ld, int64_t first_trace_id,
+                       int32_t step_seconds, int32_t kind, float peak_w, uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CAPSIM_B200_H */

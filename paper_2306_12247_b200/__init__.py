@@ -1,0 +1,85 @@
+"""paper_2306_12247_b200 — B200-native engine for the trace-driven policy-evaluation path of
+capsim (arXiv 2306.12247, "Opportunities of Renewable Energy Powered DNN Inference").
+
+A drop-in for the reference's hot path: same names, signatures and records as
+capsim/__init__.py:8-116 for profile tables, power traces, the batching / multi-tenant /
+combination policies and simulate(); every decision runs in hand-written sm_100a kernels
+(libcapsim_b200.so via ctypes). Use it as ``import paper_2306_12247_b200 as capsim``.
+
+Out of scope (not accelerated): the online controller, the sampling selector
+and the CLI.
+"""
+
+from .engine import EvalResult, HostEngine, Tables, generate_traces
+from .errors import CapsimError, ParseError, ValidationError
+from .policy import (
+    BATCHING,
+    COMBINATION,
+    IDLE_SELECTION,
+    MULTI_TENANT,
+    PolicyIndex,
+    PolicyKind,
+    PolicyTag,
+    Selection,
+    feasible_set,
+    improvement_pct,
+    sampling_policy,
+    select_config,
+    select_configs,
+    select_sampling,
+)
+from .profile import (
+    Config,
+    ProfileEntry,
+    ProfileGrid,
+    SynthParams,
+    compute_throughput,
+    grid_csv_text,
+    load_grid,
+    profiling_cost,
+    save_grid,
+    synthesize_grid,
+)
+from .sim import (
+    REPORT_SCHEMA,
+    ComparisonRow,
+    ComparisonTable,
+    SimReport,
+    StepRecord,
+    compare,
+    comparison_csv_text,
+    load_report,
+    report_from_dict,
+    report_json_text,
+    report_to_dict,
+    save_report,
+    simulate,
+    simulate_many,
+    slice_report,
+)
+from .trace import (
+    PowerTrace,
+    TraceStats,
+    load_trace,
+    normalize_display,
+    normalize_trace,
+    save_trace,
+    trace_csv_text,
+    trace_stats,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BATCHING", "COMBINATION", "MULTI_TENANT", "IDLE_SELECTION",
+    "CapsimError", "ParseError", "ValidationError",
+    "ComparisonRow", "ComparisonTable", "Config", "PolicyIndex", "PolicyKind", "PolicyTag", "PowerTrace",
+    "ProfileEntry", "ProfileGrid", "Selection", "SimReport", "StepRecord", "SynthParams", "TraceStats",
+    "REPORT_SCHEMA",
+    "compare", "comparison_csv_text", "compute_throughput", "feasible_set", "grid_csv_text", "improvement_pct",
+    "load_grid", "load_report", "load_trace", "normalize_display", "normalize_trace", "profiling_cost",
+    "report_from_dict", "report_json_text", "report_to_dict", "sampling_policy", "save_grid", "save_report",
+    "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
+    "slice_report", "synthesize_grid", "trace_csv_text", "trace_stats",
+    "Tables", "EvalResult", "HostEngine", "generate_traces",
+]

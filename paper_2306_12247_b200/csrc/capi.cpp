@@ -1,0 +1,506 @@
+// C-ABI glue: error reporting, table upload, argument validation and the host-buffer engine.
+// Each entry point's reference counterpart is documented in include/capsim_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "cs_internal.h"
+
+namespace cs {
+std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, cudaStream_t st);
+std::string eval_workspace(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, size_t* bytes);
+std::string last_kernel_ms(float* ms);
+int last_launches();
+std::string launch_select(const DevTables& v, int g, int p, const double* caps, int64_t n, int32_t* sel, int64_t* cnt,
+                          cudaStream_t st);
+std::string launch_feasible(const DevTables& v, int g, int p, const double* caps, int64_t n, uint32_t* mask,
+                            cudaStream_t st);
+std::string launch_generate(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
+                            int32_t kind, float peak, uint64_t seed, cudaStream_t st);
+
+namespace {
+thread_local std::string g_err;
+std::mutex g_upload_mu;
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+static int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+#define CS_CUDA_RET(x)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) return fail(CS_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #x ")"); \
+  } while (0)
+
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Copies the staged tables into one device allocation and fills the DevTables view.
+static int upload(Tables& t, int device, Tables::Dev** out) {
+  std::lock_guard<std::mutex> lk(g_upload_mu);
+  for (auto& d : t.devs)
+    if (d.device == device) {
+      *out = &d;
+      return CS_OK;
+    }
+  const bool f64 = t.cap_dtype == CS_CAP_F64;
+  struct Part {
+    const void* src;
+    size_t bytes;
+    size_t off;
+  };
+  std::vector<uint64_t> thr64 = f64 ? t.thresholds : std::vector<uint64_t>(1, 0);
+  Part parts[] = {
+      {t.lut.data(), t.lut.size() * 4, 0},
+      {thr64.data(), thr64.size() * 8, 0},
+      {t.vio.data(), t.vio.size() * 8, 0},
+      {t.sig.data(), t.sig.size() * 8, 0},
+      {t.umap.data(), t.umap.size() * 2, 0},
+      {t.sel.data(), t.sel.size() * 4, 0},
+      {t.sthr.data(), t.sthr.size() * 8, 0},
+      {t.spw.data(), t.spw.size() * 8, 0},
+      {t.idle_pw.data(), t.idle_pw.size() * 8, 0},
+      {t.e_off.data(), t.e_off.size() * 4, 0},
+      {t.e_mtl.data(), t.e_mtl.size() * 4, 0},
+      {t.e_bs.data(), t.e_bs.size() * 4, 0},
+      {t.e_thr.data(), t.e_thr.size() * 8, 0},
+      {t.e_pw.data(), t.e_pw.size() * 8, 0},
+  };
+  size_t total = 0;
+  for (auto& p : parts) {
+    p.off = total;
+    total += align16(p.bytes);
+  }
+  int prev = 0;
+  CS_CUDA_RET(cudaGetDevice(&prev));
+  CS_CUDA_RET(cudaSetDevice(device));
+  std::vector<unsigned char> host(total, 0);
+  for (auto& p : parts) std::memcpy(host.data() + p.off, p.src, p.bytes);
+  void* blob = nullptr;
+  cudaError_t e = cudaMalloc(&blob, total);
+  if (e == cudaSuccess) e = cudaMemcpy(blob, host.data(), total, cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    if (blob) cudaFree(blob);
+    return fail(CS_E_CUDA, std::string("CUDA error uploading tables: ") + cudaGetErrorString(e));
+  }
+  auto* b = reinterpret_cast<unsigned char*>(blob);
+  Tables::Dev d;
+  d.device = device;
+  d.blob = blob;
+  d.bytes = total;
+  DevTables& v = d.view;
+  v.cap_dtype = t.cap_dtype;
+  v.M = t.M;
+  v.U = t.U;
+  v.maxB = t.maxB;
+  v.n_lut = (int32_t)t.lut.size();
+  v.batching_mtl = t.batching_mtl;
+  v.mt_bs = t.mt_bs;
+  v.lv.lo = t.lo;
+  v.lv.hi = t.hi;
+  v.lv.kbase = t.kbase;
+  v.lv.shift1 = t.shift1;
+  v.lv.sub0 = t.n_level1;
+  v.lv.lut = reinterpret_cast<const uint32_t*>(b + parts[0].off);
+  v.lv.thr64 = reinterpret_cast<const uint64_t*>(b + parts[1].off);
+  v.vio = reinterpret_cast<const uint64_t*>(b + parts[2].off);
+  v.sig = reinterpret_cast<const uint64_t*>(b + parts[3].off);
+  v.umap = reinterpret_cast<const uint16_t*>(b + parts[4].off);
+  v.sel = reinterpret_cast<const int32_t*>(b + parts[5].off);
+  v.sthr = reinterpret_cast<const double*>(b + parts[6].off);
+  v.spw = reinterpret_cast<const double*>(b + parts[7].off);
+  v.idle_pw = reinterpret_cast<const double*>(b + parts[8].off);
+  v.e_off = reinterpret_cast<const int32_t*>(b + parts[9].off);
+  v.e_mtl = reinterpret_cast<const int32_t*>(b + parts[10].off);
+  v.e_bs = reinterpret_cast<const int32_t*>(b + parts[11].off);
+  v.e_thr = reinterpret_cast<const double*>(b + parts[12].off);
+  v.e_pw = reinterpret_cast<const double*>(b + parts[13].off);
+  t.devs.push_back(d);
+  *out = &t.devs.back();
+  return CS_OK;
+}
+
+static int current_view(const cs_tables* tp, Tables::Dev** out, int* dev) {
+  if (!tp) return fail(CS_E_INVALID, "null tables");
+  Tables& t = *reinterpret_cast<Tables*>(const_cast<cs_tables*>(tp));
+  int d = 0;
+  CS_CUDA_RET(cudaGetDevice(&d));
+  *dev = d;
+  return upload(t, d, out);
+}
+
+}  // namespace cs
+
+using cs::fail;
+using cs::Tables;
+
+extern "C" {
+
+const char* cs_last_error(void) { return cs::g_err.c_str(); }
+
+int cs_abi_version(void) { return CS_ABI_VERSION; }
+
+int cs_device_query(int32_t device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(CS_E_NODEVICE, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(CS_E_INVALID, "device ordinal out of range");
+  cudaDeviceProp p;
+  CS_CUDA_RET(cudaGetDeviceProperties(&p, device));
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  if (p.major != 10) return fail(CS_E_NODEVICE, "libcapsim_b200 is built for sm_100a (B200); found sm_" +
+                                                   std::to_string(p.major) + std::to_string(p.minor));
+  return CS_OK;
+}
+
+int cs_tables_create(const cs_grid_desc* grids, int32_t n_grids, int32_t cap_dtype, int32_t batching_mtl,
+                     int32_t multi_tenant_bs, cs_tables** out) {
+  if (!out) return fail(CS_E_INVALID, "null output pointer");
+  Tables* t = new (std::nothrow) Tables();
+  if (!t) return fail(CS_E_INVALID, "out of host memory");
+  std::string err = cs::build_tables(grids, n_grids, cap_dtype, batching_mtl, multi_tenant_bs, *t);
+  if (!err.empty()) {
+    delete t;
+    return fail(CS_E_INVALID, err);
+  }
+  *out = reinterpret_cast<cs_tables*>(t);
+  return CS_OK;
+}
+
+int cs_tables_destroy(cs_tables* tp) {
+  if (!tp) return CS_OK;
+  Tables* t = reinterpret_cast<Tables*>(tp);
+  for (auto& d : t->devs) {
+    int prev = 0;
+    if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(d.device) == cudaSuccess) {
+      cudaFree(d.blob);
+      cudaSetDevice(prev);
+    }
+  }
+  delete t;
+  return CS_OK;
+}
+
+int cs_tables_get_info(const cs_tables* tp, cs_tables_info* o) {
+  if (!tp || !o) return fail(CS_E_INVALID, "null argument");
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  o->cap_dtype = t.cap_dtype;
+  o->n_grids = t.M;
+  o->n_union_bins = t.U;
+  o->max_grid_bins = t.maxB;
+  o->lut_entries = (int32_t)t.lut.size();
+  o->lut_shift = (int32_t)t.shift1;
+  o->lut_level1 = (int32_t)t.n_level1;
+  o->lut_subtables = (int32_t)t.n_sub;
+  o->device_bytes = t.devs.empty() ? 0 : (int64_t)t.devs.front().bytes;
+  return CS_OK;
+}
+
+int cs_tables_grid_bins(const cs_tables* tp, int32_t grid, int32_t policy, int32_t* sel, int64_t* count,
+                        int32_t* n_bins) {
+  if (!tp) return fail(CS_E_INVALID, "null tables");
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (grid < 0 || grid >= t.M || policy < 0 || policy > 2) return fail(CS_E_INVALID, "grid/policy out of range");
+  const size_t o = ((size_t)grid * 3 + policy) * t.maxB;
+  const int B = t.grid_bins[grid];
+  if (sel) std::memcpy(sel, t.sel.data() + o, (size_t)B * 4);
+  if (count) std::memcpy(count, t.cnt.data() + o, (size_t)B * 8);
+  if (n_bins) *n_bins = B;
+  return CS_OK;
+}
+
+int cs_tables_union_map(const cs_tables* tp, int32_t grid, uint16_t* out) {
+  if (!tp || !out) return fail(CS_E_INVALID, "null argument");
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (grid < 0 || grid >= t.M) return fail(CS_E_INVALID, "grid out of range");
+  std::memcpy(out, t.umap.data() + (size_t)grid * t.U, (size_t)t.U * 2);
+  return CS_OK;
+}
+
+int cs_tables_lookup_host(const cs_tables* tp, const void* caps, int64_t n, int32_t* bins_out) {
+  if (!tp || (n > 0 && (!caps || !bins_out))) return fail(CS_E_INVALID, "null argument");
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (t.cap_dtype == CS_CAP_F32) {
+    const uint32_t* c = reinterpret_cast<const uint32_t*>(caps);
+    for (int64_t i = 0; i < n; ++i)
+      bins_out[i] = (int32_t)cs::bin_f32(c[i], (int32_t)t.lo, (int32_t)t.hi, t.shift1, (uint32_t)t.kbase, t.n_level1,
+                                         t.lut.data());
+  } else {
+    const uint64_t* c = reinterpret_cast<const uint64_t*>(caps);
+    for (int64_t i = 0; i < n; ++i)
+      bins_out[i] =
+          (int32_t)cs::bin_f64(c[i], t.lo, t.hi, t.shift1, t.kbase, t.n_level1, t.lut.data(), t.thresholds.data());
+  }
+  return CS_OK;
+}
+
+int cs_tables_upload(cs_tables* tp, int32_t device) {
+  if (!tp) return fail(CS_E_INVALID, "null tables");
+  Tables::Dev* d = nullptr;
+  return cs::upload(*reinterpret_cast<Tables*>(tp), device, &d);
+}
+
+static int check_eval_args(const Tables& t, const cs_eval_args* a) {
+  if (!a) return fail(CS_E_INVALID, "null args");
+  if (a->n_traces < 0 || a->n_steps < 0) return fail(CS_E_INVALID, "negative sizes");
+  if (a->n_traces > 0 && a->n_steps == 0) return fail(CS_E_INVALID, "cannot simulate an empty trace");
+  if (a->step_seconds <= 0) return fail(CS_E_INVALID, "step_seconds must be positive");
+  if (!(a->switch_penalty_s >= 0.0)) return fail(CS_E_INVALID, "switch_penalty_s must be >= 0");
+  const int vec = t.cap_dtype == CS_CAP_F32 ? 4 : 2;
+  if (a->ld < a->n_steps || a->ld % vec) return fail(CS_E_INVALID, "ld must be >= n_steps and a multiple of 16 bytes");
+  if (a->n_traces > 0 && (!a->caps || (reinterpret_cast<uintptr_t>(a->caps) & 15)))
+    return fail(CS_E_INVALID, "caps must be a 16-byte aligned device pointer");
+  if (a->step_bins && (a->ld_bins < a->n_steps || a->ld_bins % 4 || (reinterpret_cast<uintptr_t>(a->step_bins) & 7)))
+    return fail(CS_E_INVALID, "step_bins needs ld_bins >= n_steps, a multiple of 4, 8-byte alignment");
+  return CS_OK;
+}
+
+int cs_eval_workspace_size(const cs_tables* tp, const cs_eval_args* a, size_t* bytes) {
+  if (!bytes) return fail(CS_E_INVALID, "null argument");
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if ((rc = check_eval_args(t, a))) return rc;
+  std::string err = cs::eval_workspace(t, d->view, a, dev, bytes);
+  if (!err.empty()) return fail(CS_E_INVALID, err);
+  return CS_OK;
+}
+
+int cs_eval(const cs_tables* tp, const cs_eval_args* a, void* stream) {
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if ((rc = check_eval_args(t, a))) return rc;
+  if (a->n_traces == 0) return CS_OK;
+  std::string err = cs::launch_eval(t, d->view, a, dev, reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(err.rfind("CUDA", 0) == 0 ? CS_E_CUDA : CS_E_INVALID, err);
+  return CS_OK;
+}
+
+int cs_eval_last_kernel_ms(float* ms) {
+  if (!ms) return fail(CS_E_INVALID, "null argument");
+  std::string err = cs::last_kernel_ms(ms);
+  if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+int cs_eval_last_launches(int32_t* n) {
+  if (!n) return fail(CS_E_INVALID, "null argument");
+  *n = cs::last_launches();
+  return CS_OK;
+}
+
+int cs_select_caps(const cs_tables* tp, int32_t grid, int32_t policy, const double* caps_dev, int64_t n,
+                   int32_t* sel_dev, int64_t* count_dev, void* stream) {
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  if (grid < 0 || grid >= d->view.M || policy < 0 || policy > 2) return fail(CS_E_INVALID, "grid/policy out of range");
+  std::string err = cs::launch_select(d->view, grid, policy, caps_dev, n, sel_dev, count_dev,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+int cs_feasible_caps(const cs_tables* tp, int32_t grid, int32_t policy, const double* caps_dev, int64_t n,
+                     uint32_t* mask_dev, void* stream) {
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  if (grid < 0 || grid >= d->view.M || policy < 0 || policy > 2) return fail(CS_E_INVALID, "grid/policy out of range");
+  std::string err = cs::launch_feasible(d->view, grid, policy, caps_dev, n, mask_dev,
+                                        reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+int cs_generate_traces(float* caps_dev, int64_t n_traces, int64_t n_steps, int64_t ld, int64_t first_trace_id,
+                       int32_t step_seconds, int32_t kind, float peak_w, uint64_t seed, void* stream) {
+  if (ld < n_steps || n_traces < 0 || n_steps < 0 || step_seconds <= 0 || kind < 0 || kind > 3)
+    return fail(CS_E_INVALID, "bad generator arguments");
+  std::string err = cs::launch_generate(caps_dev, n_traces, n_steps, ld, first_trace_id, step_seconds, kind, peak_w,
+                                        seed, reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// host-buffer engine: chunked H2D -> eval -> D2H on three streams, double-buffered
+// ---------------------------------------------------------------------------------------------
+struct cs_engine {
+  int device = 0;
+  int cap_dtype = CS_CAP_F32;
+  int64_t chunk = 0, smax = 0;
+  cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+  void* dcaps[2] = {nullptr, nullptr};
+  cs_agg* dagg[2] = {nullptr, nullptr};
+  uint64_t* dhist = nullptr;
+  void* dws = nullptr;
+  size_t ws_bytes = 0;
+  int32_t hist_bins = 0;
+  cudaEvent_t in_done[2], cmp_done[2], out_done[2];
+};
+
+extern "C" {
+
+int cs_engine_create(int32_t device, int64_t chunk_traces_max, int64_t n_steps_max, int32_t cap_dtype,
+                     cs_engine** out) {
+  if (!out || chunk_traces_max < 1 || n_steps_max < 1) return fail(CS_E_INVALID, "bad engine arguments");
+  cs_engine* e = new (std::nothrow) cs_engine();
+  if (!e) return fail(CS_E_INVALID, "out of host memory");
+  e->device = device;
+  e->cap_dtype = cap_dtype;
+  e->chunk = chunk_traces_max;
+  e->smax = n_steps_max;
+  int prev = 0;
+  CS_CUDA_RET(cudaGetDevice(&prev));
+  CS_CUDA_RET(cudaSetDevice(device));
+  const size_t esz = cap_dtype == CS_CAP_F32 ? 4 : 8;
+  const int vec = cap_dtype == CS_CAP_F32 ? 4 : 2;
+  const int64_t ld = (n_steps_max + vec - 1) / vec * vec;
+  cudaError_t err = cudaSuccess;
+  for (int i = 0; i < 2 && err == cudaSuccess; ++i) {
+    err = cudaMalloc(&e->dcaps[i], (size_t)chunk_traces_max * ld * esz);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->in_done[i], cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->cmp_done[i], cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->out_done[i], cudaEventDisableTiming);
+  }
+  if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->s_in, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->s_cmp, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&e->s_out, cudaStreamNonBlocking);
+  cudaSetDevice(prev);
+  if (err != cudaSuccess) {
+    cs_engine_destroy(e);
+    return fail(CS_E_CUDA, std::string("CUDA error creating engine: ") + cudaGetErrorString(err));
+  }
+  *out = e;
+  return CS_OK;
+}
+
+int cs_engine_destroy(cs_engine* e) {
+  if (!e) return CS_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(e->device);
+  for (int i = 0; i < 2; ++i) {
+    if (e->dcaps[i]) cudaFree(e->dcaps[i]);
+    if (e->dagg[i]) cudaFree(e->dagg[i]);
+  }
+  if (e->dhist) cudaFree(e->dhist);
+  if (e->dws) cudaFree(e->dws);
+  if (e->s_in) cudaStreamDestroy(e->s_in);
+  if (e->s_cmp) cudaStreamDestroy(e->s_cmp);
+  if (e->s_out) cudaStreamDestroy(e->s_out);
+  cudaSetDevice(prev);
+  delete e;
+  return CS_OK;
+}
+
+int cs_engine_eval_host(cs_engine* e, const cs_tables* tp, const void* caps_host, int64_t n_traces, int64_t n_steps,
+                        int64_t ld, int32_t step_seconds, double switch_penalty_s, uint32_t flags, cs_agg* agg_host,
+                        uint64_t* hist_host, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  if (!e || !tp || !caps_host || !agg_host) return fail(CS_E_INVALID, "null argument");
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (t.cap_dtype != e->cap_dtype) return fail(CS_E_INVALID, "engine and tables cap dtype differ");
+  if (n_steps > e->smax) return fail(CS_E_INVALID, "n_steps exceeds the engine's n_steps_max");
+  int prev = 0;
+  CS_CUDA_RET(cudaGetDevice(&prev));
+  CS_CUDA_RET(cudaSetDevice(e->device));
+  const size_t esz = e->cap_dtype == CS_CAP_F32 ? 4 : 8;
+  const int64_t M = t.M;
+  const size_t agg_chunk = (size_t)e->chunk * M * 3;
+  int rc = CS_OK;
+  auto done = [&](int r) {
+    cudaSetDevice(prev);
+    return r;
+  };
+  if (!e->dagg[0]) {
+    for (int i = 0; i < 2; ++i) CS_CUDA_RET(cudaMalloc(&e->dagg[i], agg_chunk * sizeof(cs_agg)));
+  }
+  if (e->hist_bins < t.U) {
+    if (e->dhist) cudaFree(e->dhist);
+    CS_CUDA_RET(cudaMalloc(&e->dhist, (size_t)t.U * 8));
+    e->hist_bins = t.U;
+  }
+  CS_CUDA_RET(cudaMemsetAsync(e->dhist, 0, (size_t)t.U * 8, e->s_cmp));
+  // workspace for the largest chunk
+  cs_eval_args probe{};
+  probe.caps = e->dcaps[0];
+  probe.n_traces = std::min(n_traces, e->chunk);
+  probe.n_steps = n_steps;
+  probe.ld = ld;
+  probe.step_seconds = step_seconds;
+  probe.switch_penalty_s = switch_penalty_s;
+  probe.flags = flags;
+  probe.hist = e->dhist;
+  size_t need = 0;
+  if ((rc = cs_eval_workspace_size(tp, &probe, &need))) return done(rc);
+  if (need > e->ws_bytes) {
+    if (e->dws) cudaFree(e->dws);
+    CS_CUDA_RET(cudaMalloc(&e->dws, need));
+    e->ws_bytes = need;
+  }
+  int64_t h2d = 0, d2h = 0;
+  const int64_t nchunks = (n_traces + e->chunk - 1) / e->chunk;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t t0 = c * e->chunk;
+    const int64_t nt = std::min(e->chunk, n_traces - t0);
+    // H2D into buffer b once the eval that last read it is done
+    if (c >= 2) CS_CUDA_RET(cudaStreamWaitEvent(e->s_in, e->cmp_done[b], 0));
+    const size_t bytes = (size_t)nt * ld * esz;
+    CS_CUDA_RET(cudaMemcpyAsync(e->dcaps[b], reinterpret_cast<const unsigned char*>(caps_host) + (size_t)t0 * ld * esz,
+                                bytes, cudaMemcpyHostToDevice, e->s_in));
+    h2d += (int64_t)bytes;
+    CS_CUDA_RET(cudaEventRecord(e->in_done[b], e->s_in));
+    // eval once the copy landed and the previous D2H of agg[b] drained
+    CS_CUDA_RET(cudaStreamWaitEvent(e->s_cmp, e->in_done[b], 0));
+    if (c >= 2) CS_CUDA_RET(cudaStreamWaitEvent(e->s_cmp, e->out_done[b], 0));
+    cs_eval_args a = probe;
+    a.caps = e->dcaps[b];
+    a.n_traces = nt;
+    a.agg = e->dagg[b];
+    a.flags = flags | CS_FLAG_ACCUMULATE_HIST;
+    a.workspace = e->dws;
+    a.workspace_bytes = e->ws_bytes;
+    if ((rc = cs_eval(tp, &a, e->s_cmp))) return done(rc);
+    CS_CUDA_RET(cudaEventRecord(e->cmp_done[b], e->s_cmp));
+    // D2H of this chunk's aggregates
+    CS_CUDA_RET(cudaStreamWaitEvent(e->s_out, e->cmp_done[b], 0));
+    const size_t abytes = (size_t)nt * M * 3 * sizeof(cs_agg);
+    CS_CUDA_RET(cudaMemcpyAsync(agg_host + (size_t)t0 * M * 3, e->dagg[b], abytes, cudaMemcpyDeviceToHost, e->s_out));
+    d2h += (int64_t)abytes;
+    CS_CUDA_RET(cudaEventRecord(e->out_done[b], e->s_out));
+  }
+  CS_CUDA_RET(cudaStreamSynchronize(e->s_cmp));
+  if (hist_host) {
+    CS_CUDA_RET(cudaMemcpyAsync(hist_host, e->dhist, (size_t)t.U * 8, cudaMemcpyDeviceToHost, e->s_out));
+    d2h += (int64_t)t.U * 8;
+  }
+  CS_CUDA_RET(cudaStreamSynchronize(e->s_out));
+  CS_CUDA_RET(cudaStreamSynchronize(e->s_in));
+  if (h2d_bytes) *h2d_bytes = h2d;
+  if (d2h_bytes) *d2h_bytes = d2h;
+  return done(CS_OK);
+}
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+// Internal layout shared by the host staging code (staging.cpp), the kernels (kernels.cu) and
+// the C-ABI glue (capi.cpp). Not part of the public ABI (include/capsim_b200.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <deque>
+#include <vector>
+
+#include "../../include/capsim_b200.h"
+
+#if defined(__CUDACC__)
+#define CS_HD __host__ __device__ __forceinline__
+#else
+#define CS_HD inline
+#endif
+
+namespace cs {
+
+// ---------------------------------------------------------------------------------------
+// Bucketed threshold LUT.
+//
+// A cap c maps to its union bin  b(c) = #{distinct thresholds T_j : T_j <= c}  (bisect_right
+// over the merged, de-duplicated power thresholds of all grids; policy.py:139). Non-negative
+// IEEE floats order like their bit patterns, so the search runs on integer bits:
+//   u  = clamp(bits(c) as signed, LO, HI)      -0.0 (sign bit) clamps to LO -> bin 0
+//   e  = lut[(u >> S1) - KBASE]                  level-1 bucket (one shared-memory load)
+//   while e is a redirect: e = lut[SUB0 + sub*16 + ((u >> s) & 15)]   (dense clusters only)
+//   leaf: base = e >> 16;  fp32: b = base + ((e & 0xFFFF) <= (u & mask(s) & 0x3FFF))
+//                          fp64: b = base + (n(e) && T64[base] <= u)
+// Entry encoding (uint32):  hi16 = base bin | sub-table index;  lo16 =
+//   0x7FFF                 fp32 leaf, no threshold inside the bucket
+//   [0, 0x4000)            fp32 leaf, the bucket's single threshold's low bits (s <= 14)
+//   0 / 1                  fp64 leaf, number of thresholds inside the bucket
+//   0x8000 | s_next        redirect to a 16-way sub-table on bits [s_next, s_next+4)
+// ---------------------------------------------------------------------------------------
+constexpr uint32_t kLeafNone32 = 0x7FFFu;
+constexpr uint32_t kRedirect = 0x8000u;
+constexpr int kSubFan = 16;
+
+struct LutView {
+  int64_t lo, hi;      // clamp bounds on the signed bit pattern
+  uint64_t kbase;      // level-1 bucket of LO
+  uint32_t shift1;     // S1
+  uint32_t sub0;       // first sub-table entry index (= level-1 size)
+  const uint32_t* lut;
+  const uint64_t* thr64;  // fp64 thresholds (bits), fp64 tables only
+};
+
+CS_HD uint32_t bin_f32(uint32_t bits, int32_t lo, int32_t hi, uint32_t s1, uint32_t kbase, uint32_t sub0,
+                       const uint32_t* lut) {
+  int32_t si = (int32_t)bits;
+  si = si < lo ? lo : si;
+  si = si > hi ? hi : si;
+  uint32_t u = (uint32_t)si;
+  uint32_t e = lut[(u >> s1) - kbase];
+  uint32_t s = s1;
+  while (e & kRedirect) {
+    s = e & 0x1Fu;
+    e = lut[sub0 + (e >> 16) * kSubFan + ((u >> s) & 15u)];
+  }
+  uint32_t low = u & ((1u << s) - 1u) & 0x3FFFu;
+  return (e >> 16) + ((e & 0xFFFFu) <= low ? 1u : 0u);
+}
+
+CS_HD uint32_t bin_f64(uint64_t bits, int64_t lo, int64_t hi, uint32_t s1, uint64_t kbase, uint32_t sub0,
+                       const uint32_t* lut, const uint64_t* thr64) {
+  int64_t si = (int64_t)bits;
+  si = si < lo ? lo : si;
+  si = si > hi ? hi : si;
+  uint64_t u = (uint64_t)si;
+  uint32_t e = lut[(uint32_t)((u >> s1) - kbase)];
+  while (e & kRedirect) {
+    uint32_t s = e & 0x3Fu;
+    e = lut[sub0 + (e >> 16) * kSubFan + (uint32_t)((u >> s) & 15u)];
+  }
+  uint32_t base = e >> 16;
+  return base + (((e & 0x7FFFu) != 0u && thr64[base] <= u) ? 1u : 0u);
+}
+
+// Clamped bit pattern used by the violation self-check (same clamp as the lookup).
+CS_HD uint32_t clamp_bits_f32(uint32_t bits, int32_t lo, int32_t hi) {
+  int32_t si = (int32_t)bits;
+  si = si < lo ? lo : si;
+  si = si > hi ? hi : si;
+  return (uint32_t)si;
+}
+CS_HD uint64_t clamp_bits_f64(uint64_t bits, int64_t lo, int64_t hi) {
+  int64_t si = (int64_t)bits;
+  si = si < lo ? lo : si;
+  si = si > hi ? hi : si;
+  return (uint64_t)si;
+}
+
+// Device-side view of the staged tables: pointers into one device blob.
+struct DevTables {
+  int32_t cap_dtype, M, U, maxB;
+  int32_t n_lut;
+  int32_t batching_mtl, mt_bs;
+  LutView lv;
+  const uint64_t* vio;     // [U] lowest admissible cap bits per union bin (0 for bin 0)
+  const uint64_t* sig;     // [M][U] segment ids of the 3 policies, 16 bits each
+  const uint16_t* umap;    // [M][U] union bin -> grid bin
+  const int32_t* sel;      // [M][3][maxB] selected entry (caller order) or -1
+  const double* sthr;      // [M][3][maxB] selected throughput (0 when idle)
+  const double* spw;       // [M][3][maxB] selected power (0 when idle)
+  const double* idle_pw;   // [M] idle power charged to idle steps (0 when None)
+  const int32_t* e_off;    // [M+1] raw entries, caller order
+  const int32_t* e_mtl;
+  const int32_t* e_bs;
+  const double* e_thr;
+  const double* e_pw;
+};
+
+// Host-side staged tables (cs_tables in the C ABI).
+struct Tables {
+  int32_t cap_dtype = CS_CAP_F32;
+  int32_t M = 0, U = 0, maxB = 0;
+  int32_t batching_mtl = 1, mt_bs = 1;
+  std::vector<uint64_t> thresholds;   // [U-1] union thresholds (bits)
+  std::vector<int32_t> grid_bins;     // [M]
+  std::vector<uint16_t> umap;         // [M][U]
+  std::vector<int32_t> sel;           // [M][3][maxB]
+  std::vector<int64_t> cnt;           // [M][3][maxB]
+  std::vector<double> sthr, spw;      // [M][3][maxB]
+  std::vector<double> idle_pw;        // [M]
+  std::vector<uint64_t> sig;          // [M][U]
+  std::vector<uint64_t> vio;          // [U]
+  std::vector<int32_t> e_off, e_mtl, e_bs;
+  std::vector<double> e_thr, e_pw;
+  // LUT
+  int64_t lo = 0, hi = 0;
+  uint64_t kbase = 0;
+  uint32_t shift1 = 0;
+  uint32_t n_level1 = 0, n_sub = 0;
+  std::vector<uint32_t> lut;
+  // device copies (per device ordinal)
+  struct Dev {
+    int device = -1;
+    void* blob = nullptr;
+    size_t bytes = 0;
+    DevTables view{};
+  };
+  std::deque<Dev> devs;
+};
+
+std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap_dtype, int32_t batching_mtl,
+                         int32_t mt_bs, Tables& out);
+
+void set_error(const std::string& msg);
+
+}  // namespace cs

@@ -1,0 +1,288 @@
+// N1 — profile-table staging (host side).
+//
+// Restates PolicyIndex.__init__ (policy.py:118-134) for the three exhaustive regimes of every
+// grid at once and merges them into ONE rank structure, so that the per-timestep kernel does a
+// single threshold search per cap and reads all 3 policies' decisions from it:
+//
+//   * entries are sorted by (power_w, mtl, bs)                               policy.py:129
+//   * regime slices: batching = mtl == batching_mtl, multi-tenant =
+//     bs == multi_tenant_bs, combination = all                               policy.py:100-107
+//   * prefix-best with _prefer (higher ips, then lower (power, mtl, bs))     policy.py:90-97,131-134
+//   * feasible_count = bisect_right(powers, cap) = #regime entries <= cap    policy.py:139
+//
+// For every cap, all three regimes' (selection, feasible_count) depend only on how many
+// COMBINATION entries have power <= cap, i.e. on the grid bin of the cap among the grid's
+// distinct power thresholds. fp32 caps use thresholds rounded UP to fp32, which admits exactly
+// the same entries as the fp64 comparison (power <= cap  <=>  roundup32(power) <= cap for an
+// fp32 cap). Grids are merged by taking the union of their thresholds ("union bins"); each grid
+// maps union bin -> grid bin through umap.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <set>
+#include <utility>
+
+#include "cs_internal.h"
+
+namespace cs {
+namespace {
+
+uint32_t f32_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return u;
+}
+uint64_t f64_bits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, 8);
+  return u;
+}
+
+// Smallest fp32 >= d (d finite, > 0). Round-up (not round-to-nearest) keeps the comparison
+// exact: for any fp32 cap c, d <= c  <=>  roundup32(d) <= c.
+float roundup_f32(double d) {
+  float f = (float)d;
+  if ((double)f < d) f = std::nextafter(f, INFINITY);
+  return f;
+}
+
+struct Entry {
+  int32_t mtl, bs;
+  double thr, pw;
+  int32_t idx;
+  uint64_t key;  // threshold bits in the cap dtype
+};
+
+// _prefer (policy.py:90-97): true when a is preferred over b.
+bool prefer(const Entry& a, const Entry& b) {
+  if (a.thr != b.thr) return a.thr > b.thr;
+  if (a.pw != b.pw) return a.pw < b.pw;
+  if (a.mtl != b.mtl) return a.mtl < b.mtl;
+  return a.bs <= b.bs;
+}
+
+bool in_regime(int p, const Entry& e, int32_t bmtl, int32_t mbs) {
+  if (p == CS_BATCHING) return e.mtl == bmtl;
+  if (p == CS_MULTI_TENANT) return e.bs == mbs;
+  return true;
+}
+
+// ---- LUT builder -------------------------------------------------------------------------
+struct LutBuilder {
+  const std::vector<uint64_t>& T;
+  bool f32;
+  std::vector<uint32_t> sub;  // sub-table entries (appended after level 1)
+  uint32_t n_sub = 0;
+
+  LutBuilder(const std::vector<uint64_t>& t, bool is_f32) : T(t), f32(is_f32) {}
+
+  uint32_t lb(uint64_t v) const { return (uint32_t)(std::lower_bound(T.begin(), T.end(), v) - T.begin()); }
+
+  // Entry for the half-open bit range [start, start + 2^s) (start aligned to 2^s), or the
+  // single value `start` when s == 0.
+  uint32_t make(uint64_t start, uint32_t s) {
+    uint64_t end = (s >= 63) ? ~0ull : start + (1ull << s);
+    uint32_t base = lb(start);
+    uint32_t stop = (s >= 63) ? (uint32_t)T.size() : lb(end);
+    uint32_t n = stop - base;
+    if (n == 0) return (base << 16) | (f32 ? kLeafNone32 : 0u);
+    if (n == 1 && (!f32 || s <= 14)) {
+      if (f32) return (base << 16) | (uint32_t)(T[base] - start);
+      return (base << 16) | 1u;
+    }
+    uint32_t ns = s >= 4 ? s - 4 : 0;
+    uint32_t id = n_sub++;
+    size_t off = sub.size();
+    sub.resize(off + kSubFan);
+    for (uint32_t i = 0; i < (uint32_t)kSubFan; ++i) {
+      uint32_t ent;
+      if (s >= 4) {
+        ent = make(start + ((uint64_t)i << ns), ns);
+      } else {
+        uint64_t v = (start & ~15ull) | i;
+        if (v >= start && v < end) ent = make(v, 0);
+        else ent = (lb(v) << 16) | (f32 ? kLeafNone32 : 0u);  // unreachable slot
+      }
+      sub[off + i] = ent;
+    }
+    return (id << 16) | kRedirect | ns;
+  }
+};
+
+}  // namespace
+
+std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap_dtype, int32_t batching_mtl,
+                         int32_t mt_bs, Tables& out) {
+  if (cap_dtype != CS_CAP_F32 && cap_dtype != CS_CAP_F64) return "cap_dtype must be CS_CAP_F32 or CS_CAP_F64";
+  if (n_grids < 1 || grids == nullptr) return "need at least one grid";
+  const bool f32 = cap_dtype == CS_CAP_F32;
+  Tables& t = out;
+  t.cap_dtype = cap_dtype;
+  t.M = n_grids;
+  t.batching_mtl = batching_mtl;
+  t.mt_bs = mt_bs;
+
+  std::vector<std::vector<Entry>> sorted(n_grids);
+  std::vector<std::vector<uint64_t>> gthr(n_grids);
+  std::set<uint64_t> uni;
+  t.e_off.assign(1, 0);
+  for (int g = 0; g < n_grids; ++g) {
+    const cs_grid_desc& d = grids[g];
+    if (d.n_entries < 1) return "grid " + std::to_string(g) + " has no entries";
+    if (!d.mtl || !d.bs || !d.throughput_ips || !d.power_w) return "null grid array";
+    std::vector<Entry>& es = sorted[g];
+    es.resize(d.n_entries);
+    std::set<std::pair<int32_t, int32_t>> seen;
+    for (int i = 0; i < d.n_entries; ++i) {
+      Entry& e = es[i];
+      e.mtl = d.mtl[i];
+      e.bs = d.bs[i];
+      e.thr = d.throughput_ips[i];
+      e.pw = d.power_w[i];
+      e.idx = i;
+      if (e.mtl < 1 || e.bs < 1) return "mtl and bs must be >= 1";
+      if (!(std::isfinite(e.thr) && e.thr > 0)) return "throughput must be positive";
+      if (!(std::isfinite(e.pw) && e.pw > 0)) return "power must be positive";
+      if (!seen.insert({e.mtl, e.bs}).second) return "duplicate config in grid " + std::to_string(g);
+      e.key = f32 ? (uint64_t)f32_bits(roundup_f32(e.pw)) : f64_bits(e.pw);
+      t.e_mtl.push_back(e.mtl);
+      t.e_bs.push_back(e.bs);
+      t.e_thr.push_back(e.thr);
+      t.e_pw.push_back(e.pw);
+    }
+    t.e_off.push_back((int32_t)t.e_mtl.size());
+    // policy.py:129 — strict total order since (mtl, bs) is unique
+    std::sort(es.begin(), es.end(), [](const Entry& a, const Entry& b) {
+      if (a.pw != b.pw) return a.pw < b.pw;
+      if (a.mtl != b.mtl) return a.mtl < b.mtl;
+      return a.bs < b.bs;
+    });
+    for (const Entry& e : es) {
+      if (gthr[g].empty() || gthr[g].back() != e.key) gthr[g].push_back(e.key);
+      uni.insert(e.key);
+    }
+    t.idle_pw.push_back(std::isnan(d.idle_power_w) ? 0.0 : d.idle_power_w);
+  }
+  t.thresholds.assign(uni.begin(), uni.end());
+  const int64_t D = (int64_t)t.thresholds.size();
+  if (D + 1 > 65536) return "more than 65535 distinct power thresholds across grids";
+  t.U = (int32_t)(D + 1);
+  t.maxB = 0;
+  t.grid_bins.resize(n_grids);
+  for (int g = 0; g < n_grids; ++g) {
+    t.grid_bins[g] = (int32_t)gthr[g].size() + 1;
+    t.maxB = std::max(t.maxB, t.grid_bins[g]);
+  }
+  const int32_t maxB = t.maxB;
+  t.sel.assign((size_t)n_grids * 3 * maxB, -1);
+  t.cnt.assign((size_t)n_grids * 3 * maxB, 0);
+  t.sthr.assign((size_t)n_grids * 3 * maxB, 0.0);
+  t.spw.assign((size_t)n_grids * 3 * maxB, 0.0);
+  t.umap.assign((size_t)n_grids * t.U, 0);
+  t.sig.assign((size_t)n_grids * t.U, 0);
+  t.vio.assign((size_t)t.U, 0);
+
+  for (int g = 0; g < n_grids; ++g) {
+    const std::vector<Entry>& es = sorted[g];
+    const int B = t.grid_bins[g];
+    // walk the combination order once, recording every regime's prefix best/count at the end
+    // of each distinct threshold (= at each grid bin boundary)
+    int best[3] = {-1, -1, -1};
+    int64_t cnt[3] = {0, 0, 0};
+    size_t i = 0;
+    for (int b = 1; b < B; ++b) {
+      const uint64_t th = gthr[g][b - 1];
+      for (; i < es.size() && es[i].key <= th; ++i) {
+        for (int p = 0; p < 3; ++p) {
+          if (!in_regime(p, es[i], batching_mtl, mt_bs)) continue;
+          ++cnt[p];
+          if (best[p] < 0 || !prefer(es[best[p]], es[i])) best[p] = (int)i;
+        }
+      }
+      for (int p = 0; p < 3; ++p) {
+        size_t o = ((size_t)g * 3 + p) * maxB + b;
+        t.cnt[o] = cnt[p];
+        if (best[p] >= 0) {
+          const Entry& e = es[best[p]];
+          t.sel[o] = e.idx;
+          t.sthr[o] = e.thr;
+          t.spw[o] = e.pw;
+        }
+      }
+    }
+    // union bin -> grid bin, and segment ids (a policy switches configs between two steps iff
+    // their segment ids differ: prefix-best never returns to an earlier entry)
+    int32_t seg[3] = {0, 0, 0};
+    std::vector<uint64_t> gsig(B, 0);
+    for (int b = 1; b < B; ++b) {
+      for (int p = 0; p < 3; ++p) {
+        size_t o = ((size_t)g * 3 + p) * maxB;
+        if (t.sel[o + b] != t.sel[o + b - 1]) ++seg[p];
+      }
+      gsig[b] = (uint64_t)seg[0] | ((uint64_t)seg[1] << 16) | ((uint64_t)seg[2] << 32);
+    }
+    size_t j = 0;
+    for (int u = 0; u < t.U; ++u) {
+      if (u > 0) {
+        const uint64_t th = t.thresholds[u - 1];
+        while (j < gthr[g].size() && gthr[g][j] <= th) ++j;
+      }
+      uint16_t gb = (uint16_t)j;
+      t.umap[(size_t)g * t.U + u] = gb;
+      t.sig[(size_t)g * t.U + u] = gsig[gb];
+      // violation floor: the largest selected power among this grid's 3 policies
+      for (int p = 0; p < 3; ++p) {
+        size_t o = ((size_t)g * 3 + p) * maxB + gb;
+        if (t.sel[o] < 0) continue;
+        uint64_t k = f32 ? (uint64_t)f32_bits(roundup_f32(t.spw[o])) : f64_bits(t.spw[o]);
+        t.vio[u] = std::max(t.vio[u], k);
+      }
+    }
+  }
+
+  // ---- LUT over the union thresholds ----
+  const std::vector<uint64_t>& T = t.thresholds;
+  t.lo = (int64_t)T.front() - 1;
+  t.hi = (int64_t)T.back();
+  const uint32_t width = f32 ? 32 : 64;
+  const uint32_t kLevel1Max = 8192, kTotalBudget = 12288;
+  uint32_t best_s = 0;
+  size_t best_total = ~(size_t)0;
+  bool chosen = false;
+  for (uint32_t s = 0; s < width - 1; ++s) {
+    uint64_t nb = ((uint64_t)t.hi >> s) - ((uint64_t)t.lo >> s) + 1;
+    if (nb > kLevel1Max) continue;
+    LutBuilder lbld(T, f32);
+    uint64_t k0 = (uint64_t)t.lo >> s;
+    for (uint64_t k = 0; k < nb; ++k) lbld.make((k0 + k) << s, s);
+    size_t total = nb + lbld.sub.size();
+    if (total < best_total) {
+      best_total = total;
+      best_s = s;
+    }
+    if (total <= kTotalBudget) {
+      best_s = s;
+      chosen = true;
+      break;
+    }
+  }
+  (void)chosen;
+  {
+    const uint32_t s = best_s;
+    uint64_t nb = ((uint64_t)t.hi >> s) - ((uint64_t)t.lo >> s) + 1;
+    LutBuilder lbld(T, f32);
+    t.kbase = (uint64_t)t.lo >> s;
+    std::vector<uint32_t> level1(nb);
+    for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((t.kbase + k) << s, s);
+    if (lbld.n_sub > 65535) return "threshold LUT needs more than 65535 sub-tables";
+    t.shift1 = s;
+    t.n_level1 = (uint32_t)nb;
+    t.n_sub = lbld.n_sub;
+    t.lut = std::move(level1);
+    t.lut.insert(t.lut.end(), lbld.sub.begin(), lbld.sub.end());
+  }
+  return std::string();
+}
+
+}  // namespace cs
