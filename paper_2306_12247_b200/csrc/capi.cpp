@@ -454,6 +454,13 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* tp, const void* caps_host
   probe.hist = e->dhist;
   size_t need = 0;
   if ((rc = cs_eval_workspace_size(tp, &probe, &need))) return done(rc);
+  if (n_traces > e->chunk && n_traces % e->chunk) {  // the tail chunk may take the split-trace path
+    cs_eval_args tail = probe;
+    tail.n_traces = n_traces % e->chunk;
+    size_t need_tail = 0;
+    if ((rc = cs_eval_workspace_size(tp, &tail, &need_tail))) return done(rc);
+    need = std::max(need, need_tail);
+  }
   if (need > e->ws_bytes) {
     if (e->dws) cudaFree(e->dws);
     CS_CUDA_RET(cudaMalloc(&e->dws, need));
