@@ -1,0 +1,204 @@
+// B200 (sm_100a) kernels of the trace-driven policy-evaluation path.
+//
+//   select_kernel    select_config (policy.py:172-188): warp-per-cap argmax via shuffles.
+//   feasible_kernel  feasible_set (policy.py:151-169): warp-per-cap ballot bitmask.
+//   gen_kernel       synthetic solar / wind / iid cap traces (counter-based RNG).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "cs_internal.h"
+
+namespace cs {
+namespace {
+#define CS_CUDA_TRY(x)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #x ")"; \
+  } while (0)
+}  // namespace
+
+// ----------------------------------------------------------------------------------------
+// per-cap kernels (select_config / feasible_set)
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ bool regime_ok(int p, int mtl, int bs, int bmtl, int mbs) {
+  return p == CS_BATCHING ? mtl == bmtl : (p == CS_MULTI_TENANT ? bs == mbs : true);
+}
+
+// _prefer (policy.py:90-97): a preferred over b
+__device__ __forceinline__ bool prefer_dev(double ta, double pa, int ma, int ba, double tb_, double pb, int mb,
+                                           int bb) {
+  if (ta != tb_) return ta > tb_;
+  if (pa != pb) return pa < pb;
+  if (ma != mb) return ma < mb;
+  return ba <= bb;
+}
+
+__global__ void select_kernel(const DevTables tb, int g, int p, const double* __restrict__ caps, int64_t n,
+                              int32_t* __restrict__ sel_out, int64_t* __restrict__ cnt_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int e0 = tb.e_off[g], ne = tb.e_off[g + 1] - e0;
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n; q += warps) {
+    double cap = caps[q];
+    if (cap != cap) cap = INFINITY;  // bisect_right quirk: a NaN cap bisects to the end
+    int best = -1, cnt = 0;
+    double bt = 0, bp = 0;
+    int bm = 0, bbs = 0;
+    for (int j = lane; j < ne; j += 32) {
+      const int mtl = tb.e_mtl[e0 + j], bs = tb.e_bs[e0 + j];
+      const double pw = tb.e_pw[e0 + j], th = tb.e_thr[e0 + j];
+      if (!regime_ok(p, mtl, bs, tb.batching_mtl, tb.mt_bs) || !(pw <= cap)) continue;
+      ++cnt;
+      if (best < 0 || !prefer_dev(bt, bp, bm, bbs, th, pw, mtl, bs)) {
+        best = j, bt = th, bp = pw, bm = mtl, bbs = bs;
+      }
+    }
+    // warp argmax over (throughput desc, power asc, mtl asc, bs asc) with butterfly shuffles
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+      const int ob = __shfl_xor_sync(0xffffffffu, best, k);
+      const double ot = __shfl_xor_sync(0xffffffffu, bt, k), op = __shfl_xor_sync(0xffffffffu, bp, k);
+      const int om = __shfl_xor_sync(0xffffffffu, bm, k), obs = __shfl_xor_sync(0xffffffffu, bbs, k);
+      if (ob >= 0 && (best < 0 || !prefer_dev(bt, bp, bm, bbs, ot, op, om, obs))) {
+        best = ob, bt = ot, bp = op, bm = om, bbs = obs;
+      }
+    }
+    const int total = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) {
+      sel_out[q] = best;
+      cnt_out[q] = total;
+    }
+  }
+}
+
+__global__ void feasible_kernel(const DevTables tb, int g, int p, const double* __restrict__ caps, int64_t n,
+                                uint32_t* __restrict__ mask_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int e0 = tb.e_off[g], ne = tb.e_off[g + 1] - e0;
+  const int words = (ne + 31) / 32;
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n; q += warps) {
+    const double cap = caps[q];  // literal `power_w <= cap_w` (policy.py:169): NaN admits nothing
+    for (int w = 0; w < words; ++w) {
+      const int j = w * 32 + lane;
+      bool f = false;
+      if (j < ne) f = regime_ok(p, tb.e_mtl[e0 + j], tb.e_bs[e0 + j], tb.batching_mtl, tb.mt_bs) &&
+                      tb.e_pw[e0 + j] <= cap;
+      const uint32_t m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) mask_out[q * words + w] = m;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// synthetic traces
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ float u01(uint64_t h) { return (float)(h >> 40) * (1.0f / 16777216.0f); }
+__device__ __forceinline__ float gauss(uint64_t h) {
+  // Irwin-Hall(4), rescaled to unit variance: cheap and bounded
+  float s = u01(h) + u01(h * 0x9E3779B97F4A7C15ull) + u01(splitmix(h)) + u01(splitmix(h ^ 0xABCDull));
+  return (s - 2.0f) * 1.7320508f;
+}
+
+// One warp generates 32 traces (a lane each, sequential in time) and writes 32x32 tiles
+// transposed through shared memory so every store is a coalesced 128-byte row segment.
+__global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
+                           int32_t kind, float peak, uint64_t seed) {
+  __shared__ float tile[8][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32;
+  if (t0 >= T) return;
+  const int64_t tid = first_id + t0 + lane;
+  const uint64_t hk = splitmix(seed ^ splitmix((uint64_t)tid));
+  int k = kind;
+  if (k == CS_TRACE_MIXED) k = (tid & 1) ? CS_TRACE_WIND : CS_TRACE_SOLAR;
+  // per-trace parameters
+  const float var = 0.1f + 0.7f * u01(splitmix(hk ^ 1));           // Table-1 variation range 10%..80%
+  const float phase = 86400.0f * u01(splitmix(hk ^ 2));            // start time of day offset
+  const float dt = (float)step_seconds;
+  const float a_cloud = __expf(-dt / 3600.0f);                      // 1 h cloud correlation time
+  const float wind_mu = 5.0f + 5.0f * u01(splitmix(hk ^ 3));       // mean wind speed (m/s)
+  const float theta = 1.0f / 7200.0f;                               // OU mean reversion (1/s)
+  float cloud = 0.6f, wind = wind_mu;
+  for (int64_t s0 = 0; s0 < S; s0 += 32) {
+    for (int j = 0; j < 32; ++j) {
+      const int64_t s = s0 + j;
+      const uint64_t hs = splitmix(hk ^ (uint64_t)(s * 0x632BE59BD9B4E019ull));
+      float v;
+      if (k == CS_TRACE_IID) {
+        v = peak * u01(hs);
+      } else if (k == CS_TRACE_SOLAR) {
+        const float tod = fmodf(phase + (float)s * dt, 86400.0f) / 3600.0f;
+        const float clear = (tod > 6.0f && tod < 18.0f) ? __sinf(3.14159265f * (tod - 6.0f) / 12.0f) : 0.0f;
+        cloud = a_cloud * cloud + (1.0f - a_cloud) * 0.7f +
+                var * 0.5f * sqrtf(fmaxf(1.0f - a_cloud * a_cloud, 1e-6f)) * gauss(hs);
+        cloud = fminf(fmaxf(cloud, 0.2f), 1.0f);
+        v = peak * clear * cloud;
+      } else {
+        const float sdt = fminf(theta * dt, 1.0f);
+        wind = wind + sdt * (wind_mu - wind) + var * 4.0f * sqrtf(2.0f * sdt) * gauss(hs);
+        wind = fmaxf(wind, 0.0f);
+        float f = 0.0f;
+        if (wind >= 3.0f && wind < 25.0f) f = wind >= 12.0f ? 1.0f : powf((wind - 3.0f) / 9.0f, 3.0f);
+        v = peak * f;
+      }
+      tile[w][lane][j] = fminf(fmaxf(v, 0.0f), peak);
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; ++r) {
+      const int64_t tr = t0 + r;
+      const int64_t s = s0 + lane;
+      if (tr < T && s < S) caps[tr * ld + s] = tile[w][r][lane];
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// host-side launchers
+// ----------------------------------------------------------------------------------------
+void set_last_launches(int n);
+
+std::string launch_select(const DevTables& v, int g, int p, const double* caps, int64_t n, int32_t* sel, int64_t* cnt,
+                          cudaStream_t st) {
+  if (n <= 0) return std::string();
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 32);
+  select_kernel<<<(unsigned)blocks, threads, 0, st>>>(v, g, p, caps, n, sel, cnt);
+  CS_CUDA_TRY(cudaGetLastError());
+  set_last_launches(1);
+  return std::string();
+}
+
+std::string launch_feasible(const DevTables& v, int g, int p, const double* caps, int64_t n, uint32_t* mask,
+                            cudaStream_t st) {
+  if (n <= 0) return std::string();
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 32);
+  feasible_kernel<<<(unsigned)blocks, threads, 0, st>>>(v, g, p, caps, n, mask);
+  CS_CUDA_TRY(cudaGetLastError());
+  set_last_launches(1);
+  return std::string();
+}
+
+std::string launch_generate(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
+                            int32_t kind, float peak, uint64_t seed, cudaStream_t st) {
+  if (T <= 0 || S <= 0) return std::string();
+  const int64_t warps = (T + 31) / 32;
+  const int64_t blocks = (warps + 7) / 8;
+  gen_kernel<<<(unsigned)blocks, 256, 0, st>>>(caps, T, S, ld, first_id, step_seconds, kind, peak, seed);
+  CS_CUDA_TRY(cudaGetLastError());
+  return std::string();
+}
+
+}  // namespace cs

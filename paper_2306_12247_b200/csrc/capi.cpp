@@ -73,6 +73,8 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
       {t.e_bs.data(), t.e_bs.size() * 4, 0},
       {t.e_thr.data(), t.e_thr.size() * 8, 0},
       {t.e_pw.data(), t.e_pw.size() * 8, 0},
+      {t.seg_off.data(), t.seg_off.size() * 4, 0},
+      {t.seg.data(), t.seg.size() * 4, 0},
   };
   size_t total = 0;
   for (auto& p : parts) {
@@ -103,6 +105,7 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
   v.U = t.U;
   v.maxB = t.maxB;
   v.n_lut = (int32_t)t.lut.size();
+  v.n_level1 = (int32_t)t.n_level1;
   v.batching_mtl = t.batching_mtl;
   v.mt_bs = t.mt_bs;
   v.lv.lo = t.lo;
@@ -124,6 +127,8 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
   v.e_bs = reinterpret_cast<const int32_t*>(b + parts[11].off);
   v.e_thr = reinterpret_cast<const double*>(b + parts[12].off);
   v.e_pw = reinterpret_cast<const double*>(b + parts[13].off);
+  v.seg_off = reinterpret_cast<const int32_t*>(b + parts[14].off);
+  v.seg = reinterpret_cast<const int4*>(b + parts[15].off);
   t.devs.push_back(d);
   *out = &t.devs.back();
   return CS_OK;
@@ -234,7 +239,7 @@ int cs_tables_lookup_host(const cs_tables* tp, const void* caps, int64_t n, int3
   if (t.cap_dtype == CS_CAP_F32) {
     const uint32_t* c = reinterpret_cast<const uint32_t*>(caps);
     for (int64_t i = 0; i < n; ++i)
-      bins_out[i] = (int32_t)cs::bin_f32(c[i], (int32_t)t.lo, (int32_t)t.hi, t.shift1, (uint32_t)t.kbase, t.n_level1,
+      bins_out[i] = (int32_t)cs::bin_f32(c[i], t.shift1, (int32_t)t.kbase, (int32_t)t.n_level1, t.n_level1,
                                          t.lut.data());
   } else {
     const uint64_t* c = reinterpret_cast<const uint64_t*>(caps);

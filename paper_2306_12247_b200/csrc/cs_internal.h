@@ -22,45 +22,50 @@ namespace cs {
 //
 // A cap c maps to its union bin  b(c) = #{distinct thresholds T_j : T_j <= c}  (bisect_right
 // over the merged, de-duplicated power thresholds of all grids; policy.py:139). Non-negative
-// IEEE floats order like their bit patterns, so the search runs on integer bits:
-//   u  = clamp(bits(c) as signed, LO, HI)      -0.0 (sign bit) clamps to LO -> bin 0
-//   e  = lut[(u >> S1) - KBASE]                  level-1 bucket (one shared-memory load)
-//   while e is a redirect: e = lut[SUB0 + sub*16 + ((u >> s) & 15)]   (dense clusters only)
-//   leaf: base = e >> 16;  fp32: b = base + ((e & 0xFFFF) <= (u & mask(s) & 0x3FFF))
-//                          fp64: b = base + (n(e) && T64[base] <= u)
-// Entry encoding (uint32):  hi16 = base bin | sub-table index;  lo16 =
-//   0x7FFF                 fp32 leaf, no threshold inside the bucket
-//   [0, 0x4000)            fp32 leaf, the bucket's single threshold's low bits (s <= 14)
-//   0 / 1                  fp64 leaf, number of thresholds inside the bucket
-//   0x8000 | s_next        redirect to a 16-way sub-table on bits [s_next, s_next+4)
+// IEEE floats order like their bit patterns, so the search runs on integer bits.
+//
+// fp32 (the streaming path):
+//   k  = clamp((int32)bits >> S1 - KBASE, 0, NB-1)   bucket; bucket 0 and NB-1 are empty guard
+//                                                    buckets, so -0.0 / tiny caps land in bin 0
+//                                                    and caps above every threshold (and NaN)
+//                                                    in the top bin
+//   e  = lut[k]
+//   while e >= 0xFFFF0000 (redirect): s = e & 31; e = lut[SUB0 + ((e >> 5) & 0x7FF)*16 + ((bits >> s) & 15)]
+//   b  = (e + ((bits & mask(s)) << 2)) >> 16          mask(s) = (2^s - 1) & 0x3FFF
+// Leaf encoding: hi16 = base bin (thresholds below the bucket), lo16 = K where K = 0 when no
+// threshold lies in the bucket (or it sits on the bucket start: base is then +1), else
+// K = (0x4000 - (T - bucket_start)) << 2, so adding the cap's low bits carries into bit 16
+// exactly when T <= cap. One LEA + one SHF per cap.
+//
+// fp64 (drop-in PowerTrace values): u = clamp(bits, LO, HI); level-1 = (u >> S1) - KBASE;
+// leaf hi16 = base, lo16 = n in {0, 1}; b = base + (n && T64[base] <= u); redirect = 0x8000|s
+// with hi16 = sub-table index.
 // ---------------------------------------------------------------------------------------
-constexpr uint32_t kLeafNone32 = 0x7FFFu;
-constexpr uint32_t kRedirect = 0x8000u;
+constexpr uint32_t kRedirect32 = 0xFFFF0000u;  // fp32 redirect marker (hi16 == 0xFFFF)
+constexpr uint32_t kRedirect = 0x8000u;        // fp64 redirect flag
 constexpr int kSubFan = 16;
+constexpr uint32_t kMaxSub32 = 2048;
 
 struct LutView {
-  int64_t lo, hi;      // clamp bounds on the signed bit pattern
-  uint64_t kbase;      // level-1 bucket of LO
+  int64_t lo, hi;      // fp64: clamp bounds on the signed bit pattern
+  uint64_t kbase;      // level-1 bucket offset
   uint32_t shift1;     // S1
   uint32_t sub0;       // first sub-table entry index (= level-1 size)
   const uint32_t* lut;
   const uint64_t* thr64;  // fp64 thresholds (bits), fp64 tables only
 };
 
-CS_HD uint32_t bin_f32(uint32_t bits, int32_t lo, int32_t hi, uint32_t s1, uint32_t kbase, uint32_t sub0,
-                       const uint32_t* lut) {
-  int32_t si = (int32_t)bits;
-  si = si < lo ? lo : si;
-  si = si > hi ? hi : si;
-  uint32_t u = (uint32_t)si;
-  uint32_t e = lut[(u >> s1) - kbase];
+CS_HD uint32_t bin_f32(uint32_t bits, uint32_t s1, int32_t kbase, int32_t nb, uint32_t sub0, const uint32_t* lut) {
+  int32_t k = ((int32_t)bits >> s1) - kbase;
+  k = k < 0 ? 0 : k;
+  k = k > nb - 1 ? nb - 1 : k;
+  uint32_t e = lut[k];
   uint32_t s = s1;
-  while (e & kRedirect) {
-    s = e & 0x1Fu;
-    e = lut[sub0 + (e >> 16) * kSubFan + ((u >> s) & 15u)];
+  while (e >= kRedirect32) {
+    s = e & 31u;
+    e = lut[sub0 + ((e >> 5) & 0x7FFu) * kSubFan + ((bits >> s) & 15u)];
   }
-  uint32_t low = u & ((1u << s) - 1u) & 0x3FFFu;
-  return (e >> 16) + ((e & 0xFFFFu) <= low ? 1u : 0u);
+  return (e + ((bits & ((1u << s) - 1u) & 0x3FFFu) << 2)) >> 16;
 }
 
 CS_HD uint32_t bin_f64(uint64_t bits, int64_t lo, int64_t hi, uint32_t s1, uint64_t kbase, uint32_t sub0,
@@ -78,13 +83,7 @@ CS_HD uint32_t bin_f64(uint64_t bits, int64_t lo, int64_t hi, uint32_t s1, uint6
   return base + (((e & 0x7FFFu) != 0u && thr64[base] <= u) ? 1u : 0u);
 }
 
-// Clamped bit pattern used by the violation self-check (same clamp as the lookup).
-CS_HD uint32_t clamp_bits_f32(uint32_t bits, int32_t lo, int32_t hi) {
-  int32_t si = (int32_t)bits;
-  si = si < lo ? lo : si;
-  si = si > hi ? hi : si;
-  return (uint32_t)si;
-}
+// Clamped bit pattern used by the fp64 violation self-check (same clamp as the lookup).
 CS_HD uint64_t clamp_bits_f64(uint64_t bits, int64_t lo, int64_t hi) {
   int64_t si = (int64_t)bits;
   si = si < lo ? lo : si;
@@ -96,10 +95,13 @@ CS_HD uint64_t clamp_bits_f64(uint64_t bits, int64_t lo, int64_t hi) {
 struct DevTables {
   int32_t cap_dtype, M, U, maxB;
   int32_t n_lut;
+  int32_t n_level1;
   int32_t batching_mtl, mt_bs;
   LutView lv;
   const uint64_t* vio;     // [U] lowest admissible cap bits per union bin (0 for bin 0)
   const uint64_t* sig;     // [M][U] segment ids of the 3 policies, 16 bits each
+  const int32_t* seg_off;  // [M*3+1] offsets into seg
+  const int4* seg;         // selection segments per (grid, policy): {u_lo, u_hi, grid bin, 0}
   const uint16_t* umap;    // [M][U] union bin -> grid bin
   const int32_t* sel;      // [M][3][maxB] selected entry (caller order) or -1
   const double* sthr;      // [M][3][maxB] selected throughput (0 when idle)
@@ -125,6 +127,9 @@ struct Tables {
   std::vector<double> sthr, spw;      // [M][3][maxB]
   std::vector<double> idle_pw;        // [M]
   std::vector<uint64_t> sig;          // [M][U]
+  std::vector<int32_t> seg_off;       // [M*3+1]
+  std::vector<int32_t> seg;           // [n_seg][4] {u_lo, u_hi, grid bin, 0}: maximal union-bin
+                                      // runs with one selected config (policy.py:131-134 prefix best)
   std::vector<uint64_t> vio;          // [U]
   std::vector<int32_t> e_off, e_mtl, e_bs;
   std::vector<double> e_thr, e_pw;

@@ -1,0 +1,861 @@
+// N2 + N3 — the per-timestep policy kernel fused with its accumulation (sm_100a).
+//
+// Reference path: simulate() (sim.py:130-188) = PolicyIndex.select per cap (policy.py:136-148)
+// then _aggregate (sim.py:104-127), for every (trace, grid, policy).
+//
+// eval_kernel (persistent, one CTA per SM slot):
+//   * stages the threshold LUT (+ violation floors, switch signatures) into shared memory once;
+//   * worker groups of `wpg` warps each own a per-trace bin histogram in shared memory and
+//     stream their trace's caps from HBM with 128-bit non-allocating loads, 4 vectors in flight
+//     per thread;
+//   * per cap: clamp -> LUT bucket (1 LDS) -> leaf compare (rare redirect loop) -> union bin;
+//     one shared-memory atomic adds the step to the histogram; one LDS of the bin's violation
+//     floor checks power <= cap for every grid x policy (StepRecord, sim.py:50-54);
+//   * at the end of a trace the group turns the histogram into avg throughput / energy / idle /
+//     switch counts for every grid x policy. Sums run over *selection segments* (bins sharing a
+//     selection) in double-double, so the result equals the reference's exactly rounded
+//     math.fsum; the histogram also folds into the CTA's global bin histogram.
+// finalize_kernel: the same epilogue for traces split across groups (few, long traces).
+// prep_kernel: per-bin fp64 values for this launch (energy needs step_seconds, penalty needs pf).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "cs_internal.h"
+
+namespace cs {
+namespace {
+
+#define CS_CUDA_TRY(x)                                                                                  \
+  do {                                                                                                  \
+    cudaError_t e_ = (x);                                                                               \
+    if (e_ != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #x ")"; \
+  } while (0)
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// ---- double-double accumulation (error-free transforms; the build uses -fmad=false) ----
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ void dd_add2(dd& x, double p, double pe) {
+  const double s = __dadd_rn(x.hi, p);
+  const double bb = __dsub_rn(s, x.hi);
+  double e = __dadd_rn(__dsub_rn(x.hi, __dsub_rn(s, bb)), __dsub_rn(p, bb));
+  e = __dadd_rn(e, __dadd_rn(x.lo, pe));
+  const double h = __dadd_rn(s, e);
+  x.lo = __dsub_rn(e, __dsub_rn(h, s));
+  x.hi = h;
+}
+__device__ __forceinline__ void dd_add_prod(dd& x, double c, double v) {
+  const double p = __dmul_rn(c, v);
+  dd_add2(x, p, __fma_rn(c, v, -p));
+}
+
+}  // namespace
+
+struct EvalParams {
+  DevTables tb;
+  const void* caps;
+  int64_t T, S, ld;
+  int64_t seg_len;
+  int32_t nseg;
+  int32_t step_seconds;
+  uint16_t* step_bins;
+  int64_t ld_bins;
+  cs_agg* agg;
+  unsigned long long* hist;
+  uint32_t* part_hist;  // split mode: [T][U]
+  uint32_t* part_sw;    // [T][M*3][U]
+  uint32_t* part_vio;   // [T][M*3]
+  // per (grid, policy, grid bin) fp64 values of this launch, each split into {hi, mid, lo, flag}
+  // with hi/mid on a fixed quantum grid so that count x hi / count x mid accumulate EXACTLY
+  const double4* vthr;  // selected throughput (0 when idle; .w = 1 when idle)
+  const double4* vpen;  // thr * (1 - pf)
+  const double4* ven;   // (power or idle power) * step / 3600
+  double omp;
+  int32_t wpg, gpc;
+  // shared-memory layout (bytes)
+  int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
+  int32_t hstride;  // 32-bit words per histogram entry (1)
+};
+
+namespace {
+
+__device__ __forceinline__ void group_sync(int gid_local, int gsize) {
+  if (gsize == 32)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + gid_local), "r"(gsize) : "memory");
+}
+
+// prep: per grid-bin fp64 values of this launch, computed exactly like the reference per step
+// (sim.py:111, 119-122): thr, thr * (1 - pf), (power or idle) * step_seconds / 3600.
+// Each value v is split as v = hi + mid + lo with hi a multiple of Q = 2^(E+1-L) (E = exponent
+// of the table's largest value) and mid a multiple of Q*2^-L: for any count c < 2^(53-L),
+// c*hi and c*mid are exact and so are their running sums over a trace, so the epilogue needs
+// three FMAs per value instead of a double-double accumulation. One block per (grid, policy).
+__device__ __forceinline__ double4 split3(double v, int eq, int L, double flag) {
+  // eq: exponent of Q; hi = floor(v / Q) * Q, mid likewise on Q * 2^-L
+  const double hi = ldexp(floor(ldexp(v, -eq)), eq);
+  const double r = v - hi;
+  const double mid = ldexp(floor(ldexp(r, L - eq)), eq - L);
+  return make_double4(hi, mid, r - mid, flag);
+}
+
+__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, double4* vthr, double4* vpen,
+                            double4* ven) {
+  __shared__ double red[2][256];
+  const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
+  const size_t ob = (size_t)mp * B;
+  const double idle_e = __ddiv_rn(__dmul_rn(tb.idle_pw[m], step), 3600.0);
+  double mt = 0.0, me = 0.0;
+  for (int r = threadIdx.x; r < B; r += blockDim.x) {
+    const bool idle = tb.sel[ob + r] < 0;
+    mt = fmax(mt, idle ? 0.0 : tb.sthr[ob + r]);
+    me = fmax(me, idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[ob + r], step), 3600.0));
+  }
+  red[0][threadIdx.x] = mt;
+  red[1][threadIdx.x] = me;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) {
+      red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + k]);
+      red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + k]);
+    }
+    __syncthreads();
+  }
+  int et = 0, ee = 0;
+  frexp(red[0][0] > 0.0 ? red[0][0] : 1.0, &et);  // max < 2^et
+  frexp(red[1][0] > 0.0 ? red[1][0] : 1.0, &ee);
+  et -= L;
+  ee -= L;
+  for (int r = threadIdx.x; r < B; r += blockDim.x) {
+    const size_t i = ob + r;
+    if (tb.sel[i] < 0) {
+      vthr[i] = make_double4(0.0, 0.0, 0.0, 1.0);
+      vpen[i] = make_double4(0.0, 0.0, 0.0, 1.0);
+      ven[i] = split3(idle_e, ee, L, 1.0);
+    } else {
+      vthr[i] = split3(tb.sthr[i], et, L, 0.0);
+      vpen[i] = split3(__dmul_rn(tb.sthr[i], omp), et, L, 0.0);
+      ven[i] = split3(__ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee, L, 0.0);
+    }
+  }
+}
+
+// In-place inclusive prefix sum of a[0..U) by one worker group (each warp scans a contiguous
+// range, then adds the totals of the ranges before it). Raw counts are folded into ghist on
+// the way (the global config histogram).
+template <typename GH>
+__device__ __forceinline__ void group_scan(uint32_t* a, int U, GH* ghist, uint32_t* wtot, int gtid, int gsize,
+                                           int gid_local) {
+  const int lane = gtid & 31, w = gtid >> 5, nw = gsize >> 5;
+  const int per = ((U + nw - 1) / nw + 31) & ~31;
+  const int lo = min(U, w * per), hi = min(U, lo + per);
+  uint32_t carry = 0;
+  for (int base = lo; base < hi; base += 32) {
+    const int u = base + lane;
+    uint32_t x = u < hi ? a[u] : 0u;
+    if (ghist && x) atomicAdd(&ghist[u], (GH)x);
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, k);
+      if (lane >= k) x += y;
+    }
+    x += carry;
+    if (u < hi) a[u] = x;
+    carry = __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (nw > 1) {
+    if (lane == 0) wtot[w] = carry;
+    group_sync(gid_local, gsize);
+    uint32_t off = 0;
+    for (int i = 0; i < w; ++i) off += wtot[i];
+    if (off)
+      for (int u = lo + lane; u < hi; u += 32) a[u] += off;
+    group_sync(gid_local, gsize);
+  }
+}
+
+// Per-trace epilogue: every (grid, policy) aggregate of _aggregate (sim.py:104-127) from the
+// group's prefix-summed histogram. Union bins with the same selected config form a segment
+// (staged in tb.seg); a segment's step count is C[hi] - C[lo-1], so each thread handles whole
+// segments: sum += count x value in double-double (exactly rounded like math.fsum).
+//   C[u]               prefix-summed step counts (scanned in place)
+//   SW[(m*3+p)*U + u]  prefix-summed switched-step counts (PEN)
+template <bool PEN>
+__device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
+                                         const uint32_t* vcnt, double* scratch, int gtid, int gsize, int gid_local) {
+  const DevTables& tb = P.tb;
+  const int U = tb.U, M = tb.M, maxB = tb.maxB;
+  const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
+  for (int mp = 0; mp < M * 3; ++mp) {
+    const size_t ob = (size_t)mp * maxB;
+    const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
+    const uint32_t* sw = PEN ? SW + (size_t)mp * U : nullptr;
+    double th = 0.0, tm = 0.0, tl = 0.0, eh = 0.0, em = 0.0, el = 0.0;
+    long long idle = 0, swc = 0;
+    for (int k = k0 + gtid; k < k1; k += gsize) {
+      const int4 sg = __ldg(tb.seg + k);
+      const uint32_t cnt = C[sg.y] - (sg.x ? C[sg.x - 1] : 0u);
+      if (cnt == 0) continue;
+      const size_t o = ob + sg.z;
+      const double dc = (double)cnt;
+      const double4 ve = ldg4(P.ven + o);
+      eh = __fma_rn(dc, ve.x, eh);
+      em = __fma_rn(dc, ve.y, em);
+      el = __fma_rn(dc, ve.z, el);
+      uint32_t scnt = 0;
+      if (PEN) {
+        scnt = sw[sg.y] - (sg.x ? sw[sg.x - 1] : 0u);
+        swc += scnt;
+      }
+      if (ve.w != 0.0) {
+        idle += cnt;
+      } else {
+        const double4 vt = ldg4(P.vthr + o);
+        const double dn = (double)(cnt - scnt);
+        th = __fma_rn(dn, vt.x, th);
+        tm = __fma_rn(dn, vt.y, tm);
+        tl = __fma_rn(dn, vt.z, tl);
+        if (PEN && scnt) {
+          const double4 vp = ldg4(P.vpen + o);
+          const double ds = (double)scnt;
+          th = __fma_rn(ds, vp.x, th);
+          tm = __fma_rn(ds, vp.y, tm);
+          tl = __fma_rn(ds, vp.z, tl);
+        }
+      }
+    }
+    // hi / mid partial sums are exact multiples of their quanta: plain adds stay exact
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+      th = __dadd_rn(th, __shfl_xor_sync(0xffffffffu, th, k));
+      tm = __dadd_rn(tm, __shfl_xor_sync(0xffffffffu, tm, k));
+      tl = __dadd_rn(tl, __shfl_xor_sync(0xffffffffu, tl, k));
+      eh = __dadd_rn(eh, __shfl_xor_sync(0xffffffffu, eh, k));
+      em = __dadd_rn(em, __shfl_xor_sync(0xffffffffu, em, k));
+      el = __dadd_rn(el, __shfl_xor_sync(0xffffffffu, el, k));
+      idle += __shfl_xor_sync(0xffffffffu, idle, k);
+      swc += __shfl_xor_sync(0xffffffffu, swc, k);
+    }
+    if (nw > 1) {
+      if (lane == 0) {
+        double* d = scratch + wig * 8;
+        d[0] = th, d[1] = tm, d[2] = tl, d[3] = eh, d[4] = em, d[5] = el;
+        d[6] = __longlong_as_double(idle), d[7] = __longlong_as_double(swc);
+      }
+      group_sync(gid_local, gsize);
+      if (gtid == 0)
+        for (int w = 1; w < nw; ++w) {
+          const double* d = scratch + w * 8;
+          th = __dadd_rn(th, d[0]), tm = __dadd_rn(tm, d[1]), tl = __dadd_rn(tl, d[2]);
+          eh = __dadd_rn(eh, d[3]), em = __dadd_rn(em, d[4]), el = __dadd_rn(el, d[5]);
+          idle += __double_as_longlong(d[6]);
+          swc += __double_as_longlong(d[7]);
+        }
+      group_sync(gid_local, gsize);
+    }
+    if (gtid == 0 && P.agg) {
+      dd tsum{th, 0.0}, esum{eh, 0.0};
+      dd_add2(tsum, tm, 0.0);
+      dd_add2(tsum, tl, 0.0);
+      dd_add2(esum, em, 0.0);
+      dd_add2(esum, el, 0.0);
+      cs_agg a;
+      a.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
+      a.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
+      a.idle_steps = idle;
+      a.switches = swc;
+      a.violations = vcnt ? vcnt[mp] : 0;
+      a.num_steps = P.S;
+      P.agg[t * M * 3 + mp] = a;
+    }
+  }
+}
+
+// Scan + epilogue over a group histogram (smem in the main kernel, global in finalize); the
+// histogram (and switch histograms) are left zeroed for the next trace.
+template <bool PEN, typename GH>
+__device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* sw,
+                                             const uint32_t* vcnt, GH* ghist, double* scratch, int gtid, int gsize,
+                                             int gid_local) {
+  const int U = P.tb.U, M = P.tb.M;
+  uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then dd partials
+  group_scan(h, U, ghist, wtot, gtid, gsize, gid_local);
+  if (PEN)
+    for (int mp = 0; mp < M * 3; ++mp)
+      group_scan(sw + (size_t)mp * U, U, (uint32_t*)nullptr, wtot, gtid, gsize, gid_local);
+  group_sync(gid_local, gsize);
+  epilogue<PEN>(P, t, h, sw, vcnt, scratch, gtid, gsize, gid_local);
+  group_sync(gid_local, gsize);
+  for (int u = gtid; u < U; u += gsize) h[u] = 0u;
+  if (PEN)
+    for (int i = gtid; i < M * 3 * U; i += gsize) sw[i] = 0u;
+}
+
+// Exact violation recount of a segment (slow path; only runs if the fast check fired).
+template <typename CapT>
+__device__ void recount_violations(const EvalParams& P, const uint32_t* s_lut, const CapT* row, int64_t s0,
+                                   int64_t s1e, uint32_t* vcnt, int gtid, int gsize) {
+  const DevTables& tb = P.tb;
+  for (int64_t i = s0 + gtid; i < s1e; i += gsize) {
+    uint32_t b;
+    double cap;
+    if constexpr (sizeof(CapT) == 4) {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(row) + i);
+      b = bin_f32(x, tb.lv.shift1, (int32_t)tb.lv.kbase, tb.n_level1, tb.lv.sub0, s_lut);
+      cap = (double)__uint_as_float(x);
+    } else {
+      const unsigned long long x = __ldg(reinterpret_cast<const unsigned long long*>(row) + i);
+      b = bin_f64(x, tb.lv.lo, tb.lv.hi, tb.lv.shift1, tb.lv.kbase, tb.lv.sub0, s_lut, tb.lv.thr64);
+      cap = __longlong_as_double((long long)x);
+    }
+    for (int m = 0; m < tb.M; ++m) {
+      const int r = (tb.M > 1) ? (int)tb.umap[(size_t)m * tb.U + b] : (int)b;
+      for (int p = 0; p < 3; ++p) {
+        const size_t o = ((size_t)m * 3 + p) * tb.maxB + r;
+        if (tb.sel[o] >= 0 && tb.spw[o] > cap) atomicAdd(&vcnt[m * 3 + p], 1u);
+      }
+    }
+  }
+}
+
+// fp32 LUT search with its constants held in registers (encoding: cs_internal.h).
+struct Lut32 {
+  const uint32_t* lut;  // shared
+  int32_t kb, nbm1;
+  uint32_t s1, sub0, mask1;
+
+  // level-1 entry: the bucket index is clamped into [0, NB-1]; buckets 0 and NB-1 are empty
+  // guards, so -0.0 / negatives land in bin 0 and caps above every threshold in the top bin
+  __device__ __forceinline__ uint32_t entry(uint32_t x) const {
+    int32_t k = ((int32_t)x >> s1) - kb;
+    k = min(max(k, 0), nbm1);
+    return lut[k];
+  }
+  __device__ __forceinline__ static uint32_t leaf(uint32_t e, uint32_t x, uint32_t mask) {
+    return (e + ((x & mask) << 2)) >> 16;  // carries into bit 16 iff the bucket's threshold <= cap
+  }
+  __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t x) const {
+    uint32_t s = s1;
+    while (e >= kRedirect32) {
+      s = e & 31u;
+      e = lut[sub0 + ((e >> 5) & 0x7FFu) * kSubFan + ((x >> s) & 15u)];
+    }
+    return leaf(e, x, ((1u << s) - 1u) & 0x3FFFu);
+  }
+  __device__ __forceinline__ uint32_t bin(uint32_t x) const {
+    const uint32_t e = entry(x);
+    return e >= kRedirect32 ? deep(e, x) : leaf(e, x, mask1);
+  }
+};
+
+template <int VEC>
+struct VecOut;
+
+// The hot loop over one segment [s0, s1e) of trace t. Returns true if the fast violation
+// check fired (the caller then recounts exactly).
+template <bool PEN, bool STEP, bool VIO>
+__device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, const uint32_t* s_vio,
+                                                uint32_t* h, uint32_t* sw, const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
+                                                int gsize) {
+  const int U = P.tb.U, M = P.tb.M;
+  const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
+  const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
+  const int n = (int)(s1e - s0);
+  const int nvf = n >> 2;
+  bool bad = false;
+
+  auto count = [&](uint32_t b, uint32_t u) {
+    atomicAdd(&h[b], 1u);
+    if (VIO) bad |= u < s_vio[b];  // selected power of every policy must fit under the cap
+                                   // (unsigned: -0.0 and NaN patterns never trip bin 0 / top)
+  };
+  auto switches = [&](uint32_t cb, uint32_t pb) {
+    if (cb != pb)
+      for (int m = 0; m < M; ++m) {
+        const uint64_t xo = s_sig[(size_t)m * U + cb] ^ s_sig[(size_t)m * U + pb];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+          if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * U + cb], 1u);
+      }
+  };
+  auto vec4 = [&](const uint4 raw, int v) {
+    const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+    uint32_t e[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = L.entry(u[k]);
+    uint32_t b[4];
+    if (max(max(e[0], e[1]), max(e[2], e[3])) < kRedirect32) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b[k] = L.deep(e[k], u[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) count(b[k], u[k]);
+    const int64_t i0 = s0 + 4 * (int64_t)v;
+    if (PEN) {
+      uint32_t pb = b[0];  // step 0 is never penalised (sim.py:119)
+      if (i0 > 0) pb = L.bin(__ldg(row + i0 - 1));
+      switches(b[0], pb);
+      switches(b[1], b[0]);
+      switches(b[2], b[1]);
+      switches(b[3], b[2]);
+    }
+    if (STEP) {
+      uint2 o;
+      o.x = (b[0] & 0xFFFFu) | (b[1] << 16);
+      o.y = (b[2] & 0xFFFFu) | (b[3] << 16);
+      *reinterpret_cast<uint2*>(P.step_bins + t * P.ld_bins + i0) = o;
+    }
+  };
+
+  int v = gtid;
+  for (; v + 3 * gsize < nvf; v += 4 * gsize) {
+    const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
+    const uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
+    const uint4 r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16);
+    const uint4 r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
+    vec4(r0, v);
+    vec4(r1, v + gsize);
+    vec4(r2, v + 2 * gsize);
+    vec4(r3, v + 3 * gsize);
+  }
+  for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
+  // tail (< 4 caps at the very end of a trace)
+  for (int i = 4 * nvf + gtid; i < n; i += gsize) {
+    const int64_t gi = s0 + i;
+    const uint32_t u = __ldg(row + gi);
+    const uint32_t b = L.bin(u);
+    count(b, u);
+    if (PEN) switches(b, gi > 0 ? L.bin(__ldg(row + gi - 1)) : b);
+    if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
+  }
+  return bad;
+}
+
+template <bool PEN, bool STEP, bool VIO>
+__device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint32_t* s_lut, const uint64_t* s_vio,
+                                                uint32_t* h, uint32_t* sw, const uint64_t* s_sig, int64_t t,
+                                                int64_t s0, int64_t s1e, int gtid, int gsize) {
+  const DevTables& tb = P.tb;
+  const int U = tb.U, M = tb.M;
+  const unsigned long long* row = reinterpret_cast<const unsigned long long*>(P.caps) + t * P.ld;
+  const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
+  const int n = (int)(s1e - s0);
+  bool bad = false;
+  auto bin = [&](uint64_t x) {
+    return bin_f64(x, tb.lv.lo, tb.lv.hi, tb.lv.shift1, tb.lv.kbase, tb.lv.sub0, s_lut, tb.lv.thr64);
+  };
+  auto one = [&](uint64_t x, int64_t gi, uint32_t b) {
+    atomicAdd(&h[b], 1u);
+    if (VIO) bad |= clamp_bits_f64(x, tb.lv.lo, tb.lv.hi) < s_vio[b];
+    if (PEN) {
+      const uint32_t pb = gi > 0 ? bin(__ldg(row + gi - 1)) : b;
+      if (b != pb)
+        for (int m = 0; m < M; ++m) {
+          const uint64_t xo = s_sig[(size_t)m * U + b] ^ s_sig[(size_t)m * U + pb];
+          for (int p = 0; p < 3; ++p)
+            if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * U + b], 1u);
+        }
+    }
+    if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
+  };
+  const int nvf = n >> 1;
+  for (int v = gtid; v < nvf; v += gsize) {
+    const uint4 r = ldg_stream(vrow + (size_t)v * 16);
+    const uint64_t x0 = ((uint64_t)r.y << 32) | r.x, x1 = ((uint64_t)r.w << 32) | r.z;
+    const int64_t gi = s0 + 2 * (int64_t)v;
+    one(x0, gi, bin(x0));
+    one(x1, gi + 1, bin(x1));
+  }
+  if ((n & 1) && gtid == 0) {
+    const int64_t gi = s1e - 1;
+    const uint64_t x = __ldg(row + gi);
+    one(x, gi, bin(x));
+  }
+  return bad;
+}
+
+template <typename CapT, bool PEN, bool STEP, bool VIO>
+__global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ EvalParams P) {
+  constexpr bool F32 = sizeof(CapT) == 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const DevTables& tb = P.tb;
+  const int U = tb.U, M = tb.M;
+
+  // ---- N1: stage the tables into shared memory once per CTA ----
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < tb.n_lut; i += blockDim.x) s_lut[i] = __ldg(tb.lv.lut + i);
+  // violation floors: lowest admissible cap bits per union bin (u32 for fp32 tables)
+  uint64_t* s_vio = reinterpret_cast<uint64_t*>(smem + P.off_vio);
+  uint32_t* s_vio32 = reinterpret_cast<uint32_t*>(smem + P.off_vio);
+  if (VIO)
+    for (int i = threadIdx.x; i < U; i += blockDim.x) {
+      if (F32)
+        s_vio32[i] = (uint32_t)__ldg(tb.vio + i);
+      else
+        s_vio[i] = __ldg(tb.vio + i);
+    }
+  uint64_t* s_sig = reinterpret_cast<uint64_t*>(smem + P.off_sig);
+  if (PEN)
+    for (int i = threadIdx.x; i < M * U; i += blockDim.x) s_sig[i] = __ldg(tb.sig + i);
+  // CTA-level global histogram in 32-bit counters (native shared atomics); a group that would
+  // push the CTA's running step count past 2^31 first drains the counters into the global u64
+  // histogram (atomicExch, so concurrent groups lose nothing).
+  uint32_t* s_ghist = reinterpret_cast<uint32_t*>(smem + P.off_ghist);
+  uint32_t* s_gsteps = s_ghist + U;
+  const bool want_hist = P.hist != nullptr && P.nseg == 1;
+  if (want_hist) {
+    for (int i = threadIdx.x; i < U; i += blockDim.x) s_ghist[i] = 0u;
+    if (threadIdx.x == 0) *s_gsteps = 0u;
+  }
+
+  const int gsize = P.wpg * 32;
+  const int gid_local = threadIdx.x / gsize;
+  const int gtid = threadIdx.x - gid_local * gsize;
+  unsigned char* gbase = smem + P.off_groups + (size_t)gid_local * P.group_bytes;
+  uint32_t* h = reinterpret_cast<uint32_t*>(gbase);
+  uint32_t* sw = reinterpret_cast<uint32_t*>(gbase + P.off_g_sw);
+  uint32_t* vcnt = reinterpret_cast<uint32_t*>(gbase + P.off_g_vio);
+  double* scratch = reinterpret_cast<double*>(gbase + P.off_g_scr);
+  for (int u = gtid; u < U; u += gsize) h[u] = 0u;
+  if (PEN)
+    for (int i = gtid; i < M * 3 * U; i += gsize) sw[i] = 0u;
+  if (gtid < M * 3) vcnt[gtid] = 0u;
+  if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag
+  __syncthreads();
+
+  Lut32 L;
+  L.lut = s_lut;
+  L.kb = (int32_t)tb.lv.kbase;
+  L.nbm1 = tb.n_level1 - 1;
+  L.s1 = tb.lv.shift1;
+  L.sub0 = tb.lv.sub0;
+  L.mask1 = ((1u << tb.lv.shift1) - 1u) & 0x3FFFu;
+
+  const int64_t n_items = P.T * (int64_t)P.nseg;
+  const int64_t n_groups = (int64_t)gridDim.x * P.gpc;
+  for (int64_t item = (int64_t)blockIdx.x * P.gpc + gid_local; item < n_items; item += n_groups) {
+    const int64_t t = item / P.nseg;
+    const int64_t s0 = (item - t * P.nseg) * P.seg_len;
+    const int64_t s1e = min(P.S, s0 + P.seg_len);
+    bool bad;
+    if constexpr (F32)
+      bad = run_segment_f32<PEN, STEP, VIO>(P, L, s_vio32, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+    else
+      bad = run_segment_f64<PEN, STEP, VIO>(P, s_lut, s_vio, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+    if (VIO && bad) atomicOr(&vcnt[M * 3], 1u);
+    group_sync(gid_local, gsize);
+    if (VIO && vcnt[M * 3]) {  // never taken when the tables are right: exact recount
+      const CapT* row = reinterpret_cast<const CapT*>(P.caps) + t * P.ld;
+      recount_violations<CapT>(P, s_lut, row, s0, s1e, vcnt, gtid, gsize);
+      group_sync(gid_local, gsize);
+    }
+    if (P.nseg == 1) {
+      if (want_hist) {
+        uint32_t before = 0;
+        if (gtid == 0) before = atomicAdd(s_gsteps, (uint32_t)(s1e - s0));
+        before = __shfl_sync(0xffffffffu, before, 0);
+        if (before > (1u << 31)) {  // rare: drain the 32-bit counters (this warp does it)
+          if (gtid < 32) {
+            if (gtid == 0) atomicExch(s_gsteps, 0u);
+            for (int u = gtid; u < U; u += 32) {
+              const uint32_t c = atomicExch(&s_ghist[u], 0u);
+              if (c) atomicAdd(P.hist + u, (unsigned long long)c);
+            }
+          }
+        }
+      }
+      finish_trace<PEN>(P, t, h, sw, vcnt, want_hist ? s_ghist : (uint32_t*)nullptr, scratch, gtid, gsize,
+                        gid_local);
+    } else {
+      // split trace: fold this segment's partial histogram into the trace's global partials
+      for (int u = gtid; u < U; u += gsize) {
+        const uint32_t c = h[u];
+        if (c) {
+          atomicAdd(&P.part_hist[t * U + u], c);
+          h[u] = 0u;
+          if (PEN)
+            for (int mp = 0; mp < M * 3; ++mp) {
+              const uint32_t s = sw[(size_t)mp * U + u];
+              if (s) {
+                atomicAdd(&P.part_sw[(t * M * 3 + mp) * U + u], s);
+                sw[(size_t)mp * U + u] = 0u;
+              }
+            }
+        }
+      }
+      if (gtid < M * 3 && vcnt[gtid]) atomicAdd(&P.part_vio[t * M * 3 + gtid], vcnt[gtid]);
+    }
+    group_sync(gid_local, gsize);
+    if (gtid <= M * 3) vcnt[gtid] = 0u;
+    group_sync(gid_local, gsize);
+  }
+
+  if (want_hist) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < U; u += blockDim.x) {
+      const uint32_t c = s_ghist[u];
+      if (c) atomicAdd(P.hist + u, (unsigned long long)c);
+    }
+  }
+}
+
+template <bool PEN>
+__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EvalParams P) {
+  __shared__ double scratch[8 * 8];
+  const int64_t t = blockIdx.x;
+  const int U = P.tb.U, M = P.tb.M;
+  uint32_t* h = P.part_hist + t * U;
+  uint32_t* sw = PEN ? P.part_sw + t * (int64_t)M * 3 * U : nullptr;
+  const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
+  finish_trace<PEN>(P, t, h, sw, vc, P.hist, scratch, threadIdx.x, blockDim.x, 0);
+}
+
+// ----------------------------------------------------------------------------------------
+// host side: launch planning
+// ----------------------------------------------------------------------------------------
+thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
+thread_local int g_last_launches = 0;
+thread_local bool g_timed = false;
+
+struct Plan {
+  int threads, wpg, gpc, ctas;
+  int32_t nseg;
+  int64_t seg_len;
+  size_t smem;
+  size_t ws_prep, ws_split;
+  EvalParams P;
+};
+
+int sm_count(int dev) {
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev];
+}
+
+template <typename CapT, bool PEN, bool STEP, bool VIO>
+void* kptr() {
+  return (void*)eval_kernel<CapT, PEN, STEP, VIO>;
+}
+
+void* pick_kernel(bool f32, bool pen, bool step, bool vio) {
+#define CS_K(A, B, C) \
+  if (pen == A && step == B && vio == C) return f32 ? kptr<float, A, B, C>() : kptr<double, A, B, C>();
+  CS_K(false, false, false)
+  CS_K(false, false, true)
+  CS_K(false, true, false)
+  CS_K(false, true, true)
+  CS_K(true, false, false)
+  CS_K(true, false, true)
+  CS_K(true, true, false)
+  CS_K(true, true, true)
+#undef CS_K
+  return nullptr;
+}
+
+size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, Plan& pl) {
+  const bool f32 = t.cap_dtype == CS_CAP_F32;
+  const bool pen = a->switch_penalty_s > 0.0;
+  const bool vio = (a->flags & CS_FLAG_CHECK_VIOLATIONS) != 0;
+  void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio);
+  const int U = t.U, M = t.M;
+  int smem_optin = 232448;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int nsm = sm_count(dev);
+  const size_t lut_bytes = a16((size_t)t.lut.size() * 4);
+  const size_t vio_bytes = vio ? a16((size_t)U * (f32 ? 4 : 8)) : 0;
+  const size_t sig_bytes = pen ? a16((size_t)M * U * 8) : 0;
+  const size_t gh_bytes = a->hist ? a16((size_t)U * 4 + 4) : 0;
+  const size_t fixed = lut_bytes + vio_bytes + sig_bytes + gh_bytes;
+  const int hs = 1;
+  auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
+    size_t gb = a16((size_t)U * 4 * hs);
+    *off_sw = gb;
+    gb += pen ? a16((size_t)M * 3 * U * 4) : 0;
+    *off_v = gb;
+    gb += a16((size_t)(M * 3 + 1) * 4);
+    *off_scr = gb;
+    gb += (size_t)wpg * 8 * 8;
+    return a16(gb);
+  };
+  // candidates: most resident warps per SM first, then the smallest worker group
+  int best_warps = -1, b_threads = 0, b_wpg = 0, b_per_sm = 0;
+  size_t b_smem = 0;
+  for (int threads : {512, 256, 128}) {
+    for (int wpg : {1, 2, 4, 8, 16}) {
+      const int wpc = threads / 32;
+      if (wpg > wpc) continue;
+      const int gpc = wpc / wpg;
+      if (wpg > 1 && gpc > 15) continue;  // named barriers 1..15
+      size_t o1, o2, o3;
+      const size_t smem = fixed + (size_t)gpc * group_bytes(wpg, &o1, &o2, &o3);
+      if (smem > (size_t)smem_optin) continue;
+      int per_sm = 0;
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (per_sm < 1) continue;
+      const int warps = per_sm * wpc;
+      if (warps > best_warps || (warps == best_warps && wpg < b_wpg)) {
+        best_warps = warps, b_threads = threads, b_wpg = wpg, b_per_sm = per_sm, b_smem = smem;
+      }
+    }
+  }
+  if (best_warps < 0)
+    return "tables too large for shared memory (" + std::to_string(U) + " union bins, " +
+           std::to_string(t.lut.size()) + " LUT entries)";
+  pl.threads = b_threads;
+  pl.wpg = b_wpg;
+  pl.gpc = b_threads / 32 / b_wpg;
+  pl.smem = b_smem;
+  const int64_t groups_total = (int64_t)nsm * b_per_sm * pl.gpc;
+  int64_t nseg = 1;
+  if (a->n_traces < 2 * groups_total) {  // too few traces to fill the machine: split them
+    const int64_t want = (2 * groups_total + a->n_traces - 1) / std::max<int64_t>(a->n_traces, 1);
+    nseg = std::max<int64_t>(1, std::min(want, std::max<int64_t>(1, a->n_steps / 2048)));
+  }
+  int64_t seg_len = (a->n_steps + nseg - 1) / nseg;
+  seg_len = (seg_len + 127) / 128 * 128;
+  nseg = (a->n_steps + seg_len - 1) / seg_len;
+  pl.nseg = (int32_t)nseg;
+  pl.seg_len = seg_len;
+  pl.ctas = (int)std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)nsm * b_per_sm, (a->n_traces * nseg + pl.gpc - 1) / pl.gpc));
+  pl.ws_prep = a16((size_t)M * 3 * t.maxB * 32) * 3;
+  pl.ws_split = nseg > 1 ? (size_t)a->n_traces *
+                               ((size_t)U + (pen ? (size_t)M * 3 * U : 0) + (size_t)M * 3) * sizeof(uint32_t)
+                         : 0;
+
+  EvalParams& P = pl.P;
+  P = EvalParams{};
+  P.tb = view;
+  P.caps = a->caps;
+  P.T = a->n_traces;
+  P.S = a->n_steps;
+  P.ld = a->ld;
+  P.seg_len = seg_len;
+  P.nseg = (int32_t)nseg;
+  P.step_seconds = a->step_seconds;
+  {
+    const double step = (double)a->step_seconds;
+    const double pen_s = a->switch_penalty_s < step ? a->switch_penalty_s : step;  // sim.py:111
+    P.omp = 1.0 - pen_s / step;
+  }
+  P.step_bins = a->step_bins;
+  P.ld_bins = a->ld_bins;
+  P.agg = a->agg;
+  P.hist = reinterpret_cast<unsigned long long*>(a->hist);
+  P.wpg = pl.wpg;
+  P.gpc = pl.gpc;
+  P.hstride = hs;
+  P.off_vio = (int32_t)lut_bytes;
+  P.off_sig = (int32_t)(lut_bytes + vio_bytes);
+  P.off_ghist = (int32_t)(lut_bytes + vio_bytes + sig_bytes);
+  P.off_groups = (int32_t)fixed;
+  size_t o1, o2, o3;
+  P.group_bytes = (int32_t)group_bytes(pl.wpg, &o1, &o2, &o3);
+  P.off_g_sw = (int32_t)o1;
+  P.off_g_vio = (int32_t)o2;
+  P.off_g_scr = (int32_t)o3;
+  return std::string();
+}
+
+}  // namespace
+
+void set_last_launches(int n) { g_last_launches = n; }
+
+std::string eval_workspace(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, size_t* bytes) {
+  Plan pl;
+  std::string err = make_plan(t, view, a, dev, pl);
+  if (!err.empty()) return err;
+  *bytes = pl.ws_prep + pl.ws_split;
+  return std::string();
+}
+
+std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, cudaStream_t st) {
+  Plan pl;
+  std::string err = make_plan(t, view, a, dev, pl);
+  if (!err.empty()) return err;
+  const bool f32 = t.cap_dtype == CS_CAP_F32;
+  const bool pen = a->switch_penalty_s > 0.0;
+  const bool vio = (a->flags & CS_FLAG_CHECK_VIOLATIONS) != 0;
+  EvalParams& P = pl.P;
+  const size_t need = pl.ws_prep + pl.ws_split;
+  if (a->workspace == nullptr || a->workspace_bytes < need)
+    return "workspace too small: need " + std::to_string(need) + " bytes (cs_eval_workspace_size)";
+  unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace);
+  const size_t nv = (size_t)t.M * 3 * t.maxB;
+  double4* vthr = reinterpret_cast<double4*>(ws);
+  double4* vpen = reinterpret_cast<double4*>(ws + a16(nv * 32));
+  double4* ven = reinterpret_cast<double4*>(ws + 2 * a16(nv * 32));
+  P.vthr = vthr, P.vpen = vpen, P.ven = ven;
+  // bits per exact level: counts up to S must keep count x hi below 2^53 quanta
+  int L = 26;
+  while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
+  int launches = 0;
+  prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, vthr, vpen, ven);
+  CS_CUDA_TRY(cudaGetLastError());
+  ++launches;
+  if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
+  if (pl.nseg > 1) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);
+    P.part_hist = w;
+    P.part_sw = w + (size_t)a->n_traces * t.U;
+    P.part_vio = P.part_sw + (pen ? (size_t)a->n_traces * t.M * 3 * t.U : 0);
+    CS_CUDA_TRY(cudaMemsetAsync(w, 0, pl.ws_split, st));
+  }
+  void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio);
+  CS_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  if (!g_ev0) {
+    CS_CUDA_TRY(cudaEventCreate(&g_ev0));
+    CS_CUDA_TRY(cudaEventCreate(&g_ev1));
+  }
+  CS_CUDA_TRY(cudaEventRecord(g_ev0, st));
+  void* args[] = {(void*)&P};
+  CS_CUDA_TRY(cudaLaunchKernel(fn, dim3(pl.ctas), dim3(pl.threads), args, pl.smem, st));
+  CS_CUDA_TRY(cudaEventRecord(g_ev1, st));
+  g_timed = true;
+  ++launches;
+  if (pl.nseg > 1) {
+    void* ff = pen ? (void*)finalize_kernel<true> : (void*)finalize_kernel<false>;
+    CS_CUDA_TRY(cudaLaunchKernel(ff, dim3((unsigned)a->n_traces), dim3(256), args, 0, st));
+    ++launches;
+  }
+  g_last_launches = launches;
+  return std::string();
+}
+
+std::string last_kernel_ms(float* ms) {
+  if (!g_timed) return "no cs_eval launch on this thread yet";
+  CS_CUDA_TRY(cudaEventElapsedTime(ms, g_ev0, g_ev1));
+  return std::string();
+}
+
+int last_launches() { return g_last_launches; }
+
+}  // namespace cs

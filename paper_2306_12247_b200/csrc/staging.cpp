@@ -80,16 +80,22 @@ struct LutBuilder {
   uint32_t lb(uint64_t v) const { return (uint32_t)(std::lower_bound(T.begin(), T.end(), v) - T.begin()); }
 
   // Entry for the half-open bit range [start, start + 2^s) (start aligned to 2^s), or the
-  // single value `start` when s == 0.
+  // single value `start` when s == 0. Encodings: see cs_internal.h.
   uint32_t make(uint64_t start, uint32_t s) {
     uint64_t end = (s >= 63) ? ~0ull : start + (1ull << s);
     uint32_t base = lb(start);
     uint32_t stop = (s >= 63) ? (uint32_t)T.size() : lb(end);
     uint32_t n = stop - base;
-    if (n == 0) return (base << 16) | (f32 ? kLeafNone32 : 0u);
-    if (n == 1 && (!f32 || s <= 14)) {
-      if (f32) return (base << 16) | (uint32_t)(T[base] - start);
-      return (base << 16) | 1u;
+    if (f32) {
+      if (n == 0) return base << 16;
+      if (n == 1 && s <= 14) {
+        const uint32_t tl = (uint32_t)(T[base] - start);
+        if (tl == 0) return (base + 1) << 16;  // threshold on the bucket start: every cap is above
+        return (base << 16) | ((0x4000u - tl) << 2);
+      }
+    } else {
+      if (n == 0) return base << 16;
+      if (n == 1) return (base << 16) | 1u;
     }
     uint32_t ns = s >= 4 ? s - 4 : 0;
     uint32_t id = n_sub++;
@@ -102,10 +108,11 @@ struct LutBuilder {
       } else {
         uint64_t v = (start & ~15ull) | i;
         if (v >= start && v < end) ent = make(v, 0);
-        else ent = (lb(v) << 16) | (f32 ? kLeafNone32 : 0u);  // unreachable slot
+        else ent = lb(v) << 16;  // unreachable slot
       }
       sub[off + i] = ent;
     }
+    if (f32) return kRedirect32 | (id << 5) | ns;
     return (id << 16) | kRedirect | ns;
   }
 };
@@ -241,41 +248,72 @@ std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap
     }
   }
 
+  // ---- selection segments: maximal runs of union bins sharing a selection, per (grid, policy).
+  // The epilogue sums count x value once per segment instead of once per bin.
+  t.seg_off.assign(1, 0);
+  for (int g = 0; g < n_grids; ++g) {
+    for (int p = 0; p < 3; ++p) {
+      int u = 0;
+      while (u < t.U) {
+        const uint64_t sid = (t.sig[(size_t)g * t.U + u] >> (16 * p)) & 0xFFFFull;
+        int v = u;
+        while (v + 1 < t.U && ((t.sig[(size_t)g * t.U + v + 1] >> (16 * p)) & 0xFFFFull) == sid) ++v;
+        t.seg.insert(t.seg.end(), {u, v, (int32_t)t.umap[(size_t)g * t.U + u], 0});
+        u = v + 1;
+      }
+      t.seg_off.push_back((int32_t)(t.seg.size() / 4));
+    }
+  }
+
   // ---- LUT over the union thresholds ----
+  // fp32: level-1 buckets k = (bits >> S1) - KBASE with an empty guard bucket below the first
+  // threshold and one above the last (the kernel clamps k, not the cap). fp64: clamp the cap.
   const std::vector<uint64_t>& T = t.thresholds;
   t.lo = (int64_t)T.front() - 1;
   t.hi = (int64_t)T.back();
   const uint32_t width = f32 ? 32 : 64;
   const uint32_t kLevel1Max = 8192, kTotalBudget = 12288;
-  uint32_t best_s = 0;
+  auto range = [&](uint32_t s, uint64_t* kb, uint64_t* nb) -> bool {
+    if (f32) {
+      // s >= 1 keeps ((int32)bits >> s) - KBASE free of int32 overflow for sign-bit patterns
+      if (s == 0 || (T.front() >> s) == 0) return false;  // and leaves room for the guard bucket
+      *kb = (T.front() >> s) - 1;
+      *nb = (T.back() >> s) - *kb + 2;
+    } else {
+      *kb = (uint64_t)t.lo >> s;
+      *nb = ((uint64_t)t.hi >> s) - *kb + 1;
+    }
+    return true;
+  };
+  uint32_t best_s = width - 2;
   size_t best_total = ~(size_t)0;
-  bool chosen = false;
-  for (uint32_t s = 0; s < width - 1; ++s) {
-    uint64_t nb = ((uint64_t)t.hi >> s) - ((uint64_t)t.lo >> s) + 1;
-    if (nb > kLevel1Max) continue;
+  for (uint32_t s = 0; s + 1 < width; ++s) {
+    if (f32 && s > 30) break;
+    uint64_t kb, nb;
+    if (!range(s, &kb, &nb) || nb > kLevel1Max) continue;
     LutBuilder lbld(T, f32);
-    uint64_t k0 = (uint64_t)t.lo >> s;
-    for (uint64_t k = 0; k < nb; ++k) lbld.make((k0 + k) << s, s);
-    size_t total = nb + lbld.sub.size();
-    if (total < best_total) {
+    for (uint64_t k = 0; k < nb; ++k) lbld.make((kb + k) << s, s);
+    const size_t total = nb + lbld.sub.size();
+    if (total < best_total && !(f32 && lbld.n_sub > kMaxSub32)) {
       best_total = total;
       best_s = s;
     }
-    if (total <= kTotalBudget) {
+    if (total <= kTotalBudget && !(f32 && lbld.n_sub > kMaxSub32)) {
       best_s = s;
-      chosen = true;
       break;
     }
   }
-  (void)chosen;
   {
     const uint32_t s = best_s;
-    uint64_t nb = ((uint64_t)t.hi >> s) - ((uint64_t)t.lo >> s) + 1;
+    uint64_t kb, nb;
+    if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
     LutBuilder lbld(T, f32);
-    t.kbase = (uint64_t)t.lo >> s;
+    t.kbase = kb;
     std::vector<uint32_t> level1(nb);
-    for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((t.kbase + k) << s, s);
+    for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
+    if (f32 && lbld.n_sub > kMaxSub32) return "threshold LUT needs more than 2048 sub-tables";
     if (lbld.n_sub > 65535) return "threshold LUT needs more than 65535 sub-tables";
+    if (f32 && t.U > 65535) return "more than 65534 distinct power thresholds across grids";
     t.shift1 = s;
     t.n_level1 = (uint32_t)nb;
     t.n_sub = lbld.n_sub;

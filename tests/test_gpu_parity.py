@@ -258,3 +258,25 @@ def test_host_engine_matches_device_path(cs, torch):
     assert torch.equal(hist, dev.hist.cpu())
     assert h2d == caps.nbytes
     assert d2h == agg.numel() * 8 + hist.numel() * 8
+
+
+def test_engine_special_caps_match_host_lookup(cs, torch):
+    """-0.0, denormals, +inf, NaN and huge caps through the device LUT == host restatement ==
+    bisect_right semantics (NaN and +inf bisect to the top, policy.py:139)."""
+    g = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
+    special = np.array([-0.0, 0.0, 1e-45, 1e-38, 59.99, 60.0, 349.9999, 350.0, 350.0001, 3e38,
+                        np.inf, np.nan], np.float32)
+    rng = np.random.default_rng(5)
+    pws = np.array(g.columns()[4], np.float64)
+    near = np.concatenate([pws.astype(np.float32), np.nextafter(pws.astype(np.float32), np.float32(0))])
+    caps = np.concatenate([special, near, rng.uniform(0, 360, 4000).astype(np.float32)])
+    S = caps.shape[0]
+    host = np.zeros((1, (S + 3) // 4 * 4), np.float32)
+    host[0, :S] = caps
+    t = cs.Tables.stage([g], "f32")
+    res = t.evaluate(torch.from_numpy(host).cuda(), S, step_seconds=60, per_step=True)
+    dev_bins = res.bins_numpy(0)
+    assert np.array_equal(dev_bins, t.lookup_host(caps))
+    top = t.n_union_bins - 1
+    assert dev_bins[0] == 0 and dev_bins[1] == 0 and dev_bins[10] == top and dev_bins[11] == top
+    assert int(res.violations.sum()) == 0
