@@ -76,6 +76,10 @@ typedef struct {
   int32_t lut_level1;
   int32_t lut_subtables;
   int64_t device_bytes;    /* size of the staged device blob */
+  int32_t lut_unsafe_leaves; /* fp32: LUT leaves whose selections are NOT proven to fit every cap
+                                they serve (0 for well-formed tables; such leaves take the exact
+                                per-step power check) */
+  int32_t n_segments;      /* selection segments over all grids x policies */
 } cs_tables_info;
 
 typedef struct cs_tables cs_tables;

@@ -83,6 +83,8 @@ class TablesInfo(C.Structure):
         ("lut_level1", C.c_int32),
         ("lut_subtables", C.c_int32),
         ("device_bytes", C.c_int64),
+        ("lut_unsafe_leaves", C.c_int32),
+        ("n_segments", C.c_int32),
     ]
 
 

@@ -209,6 +209,8 @@ int cs_tables_get_info(const cs_tables* tp, cs_tables_info* o) {
   o->lut_level1 = (int32_t)t.n_level1;
   o->lut_subtables = (int32_t)t.n_sub;
   o->device_bytes = t.devs.empty() ? 0 : (int64_t)t.devs.front().bytes;
+  o->lut_unsafe_leaves = (int32_t)t.n_unsafe;
+  o->n_segments = (int32_t)(t.seg.size() / 4);
   return CS_OK;
 }
 

@@ -35,7 +35,9 @@ namespace cs {
 // Leaf encoding: hi16 = base bin (thresholds below the bucket), lo16 = K where K = 0 when no
 // threshold lies in the bucket (or it sits on the bucket start: base is then +1), else
 // K = (0x4000 - (T - bucket_start)) << 2, so adding the cap's low bits carries into bit 16
-// exactly when T <= cap. One LEA + one SHF per cap.
+// exactly when T <= cap. One LEA + one SHF per cap. Bit 0 (K is a multiple of 4) marks a leaf
+// that is NOT proven violation-free (selected power <= every cap it serves): the kernel's
+// per-step power check is an OR of that bit, with an exact recount when it is ever set.
 //
 // fp64 (drop-in PowerTrace values): u = clamp(bits, LO, HI); level-1 = (u >> S1) - KBASE;
 // leaf hi16 = base, lo16 = n in {0, 1}; b = base + (n && T64[base] <= u); redirect = 0x8000|s
@@ -138,6 +140,7 @@ struct Tables {
   uint64_t kbase = 0;
   uint32_t shift1 = 0;
   uint32_t n_level1 = 0, n_sub = 0;
+  uint32_t n_unsafe = 0;  // fp32 leaves not proven violation-free (0 for well-formed tables)
   std::vector<uint32_t> lut;
   // device copies (per device ordinal)
   struct Dev {

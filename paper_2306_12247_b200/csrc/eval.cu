@@ -82,11 +82,11 @@ struct EvalParams {
   uint32_t* part_hist;  // split mode: [T][U]
   uint32_t* part_sw;    // [T][M*3][U]
   uint32_t* part_vio;   // [T][M*3]
-  // per (grid, policy, grid bin) fp64 values of this launch, each split into {hi, mid, lo, flag}
-  // with hi/mid on a fixed quantum grid so that count x hi / count x mid accumulate EXACTLY
-  const double4* vthr;  // selected throughput (0 when idle; .w = 1 when idle)
-  const double4* vpen;  // thr * (1 - pf)
-  const double4* ven;   // (power or idle power) * step / 3600
+  // per selection segment of this launch: {u_lo, u_hi, idle, -} then thr / energy / penalised thr,
+  // each split into {hi, mid, lo} with hi and mid on fixed quantum grids so that count x hi and
+  // count x mid accumulate EXACTLY (6 x 16 B per segment, see prep_kernel)
+  const double2* segrec;
+  int32_t U4;  // histogram row stride (U rounded up to a multiple of 4)
   double omp;
   int32_t wpg, gpc;
   // shared-memory layout (bytes)
@@ -103,22 +103,23 @@ __device__ __forceinline__ void group_sync(int gid_local, int gsize) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + gid_local), "r"(gsize) : "memory");
 }
 
-// prep: per grid-bin fp64 values of this launch, computed exactly like the reference per step
-// (sim.py:111, 119-122): thr, thr * (1 - pf), (power or idle) * step_seconds / 3600.
+// prep: per selection segment, the fp64 values of this launch computed exactly like the
+// reference per step (sim.py:111, 119-122): thr, thr * (1 - pf), (power or idle) * step / 3600.
 // Each value v is split as v = hi + mid + lo with hi a multiple of Q = 2^(E+1-L) (E = exponent
-// of the table's largest value) and mid a multiple of Q*2^-L: for any count c < 2^(53-L),
-// c*hi and c*mid are exact and so are their running sums over a trace, so the epilogue needs
-// three FMAs per value instead of a double-double accumulation. One block per (grid, policy).
-__device__ __forceinline__ double4 split3(double v, int eq, int L, double flag) {
-  // eq: exponent of Q; hi = floor(v / Q) * Q, mid likewise on Q * 2^-L
-  const double hi = ldexp(floor(ldexp(v, -eq)), eq);
+// of the (grid, policy) table's largest value) and mid a multiple of Q*2^-L: for any count
+// c < 2^(53-L), c*hi and c*mid are exact and so are their running sums over a trace, so the
+// epilogue needs three FMAs per value instead of a double-double accumulation.
+// One block per (grid, policy).
+__device__ __forceinline__ void split3(double v, int eq, int L, double* out) {
+  const double hi = ldexp(floor(ldexp(v, -eq)), eq);  // floor(v / Q) * Q, exact
   const double r = v - hi;
   const double mid = ldexp(floor(ldexp(r, L - eq)), eq - L);
-  return make_double4(hi, mid, r - mid, flag);
+  out[0] = hi;
+  out[1] = mid;
+  out[2] = r - mid;
 }
 
-__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, double4* vthr, double4* vpen,
-                            double4* ven) {
+__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, double2* segrec) {
   __shared__ double red[2][256];
   const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
   const size_t ob = (size_t)mp * B;
@@ -144,42 +145,60 @@ __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, 
   frexp(red[1][0] > 0.0 ? red[1][0] : 1.0, &ee);
   et -= L;
   ee -= L;
-  for (int r = threadIdx.x; r < B; r += blockDim.x) {
-    const size_t i = ob + r;
-    if (tb.sel[i] < 0) {
-      vthr[i] = make_double4(0.0, 0.0, 0.0, 1.0);
-      vpen[i] = make_double4(0.0, 0.0, 0.0, 1.0);
-      ven[i] = split3(idle_e, ee, L, 1.0);
-    } else {
-      vthr[i] = split3(tb.sthr[i], et, L, 0.0);
-      vpen[i] = split3(__dmul_rn(tb.sthr[i], omp), et, L, 0.0);
-      ven[i] = split3(__ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee, L, 0.0);
-    }
+  const int k0 = tb.seg_off[mp], k1 = tb.seg_off[mp + 1];
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    const int4 sg = tb.seg[k];
+    const size_t i = ob + sg.z;
+    const bool idle = tb.sel[i] < 0;
+    double v[12];
+    split3(idle ? 0.0 : tb.sthr[i], et, L, v + 0);
+    split3(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee, L, v + 3);
+    split3(idle ? 0.0 : __dmul_rn(tb.sthr[i], omp), et, L, v + 6);
+    v[9] = 0.0;
+    double2* out = segrec + (size_t)k * 6;
+    int4 head = make_int4(sg.x, sg.y, idle ? 1 : 0, 0);
+    out[0] = *reinterpret_cast<const double2*>(&head);
+    out[1] = make_double2(v[0], v[1]);   // thr hi, mid
+    out[2] = make_double2(v[2], v[3]);   // thr lo, en hi
+    out[3] = make_double2(v[4], v[5]);   // en mid, lo
+    out[4] = make_double2(v[6], v[7]);   // pen hi, mid
+    out[5] = make_double2(v[8], v[9]);   // pen lo
   }
 }
 
-// In-place inclusive prefix sum of a[0..U) by one worker group (each warp scans a contiguous
-// range, then adds the totals of the ranges before it). Raw counts are folded into ghist on
-// the way (the global config histogram).
+// In-place inclusive prefix sum of a[0..U4) by one worker group, 4 bins per lane (LDS.128):
+// each warp scans a contiguous range, then adds the totals of the ranges before it. Raw counts
+// are folded into ghist on the way (the global config histogram).
 template <typename GH>
-__device__ __forceinline__ void group_scan(uint32_t* a, int U, GH* ghist, uint32_t* wtot, int gtid, int gsize,
+__device__ __forceinline__ void group_scan(uint32_t* a, int U4, GH* ghist, uint32_t* wtot, int gtid, int gsize,
                                            int gid_local) {
   const int lane = gtid & 31, w = gtid >> 5, nw = gsize >> 5;
-  const int per = ((U + nw - 1) / nw + 31) & ~31;
-  const int lo = min(U, w * per), hi = min(U, lo + per);
+  const int per = ((U4 + nw - 1) / nw + 127) & ~127;
+  const int lo = min(U4, w * per), hi = min(U4, lo + per);
   uint32_t carry = 0;
-  for (int base = lo; base < hi; base += 32) {
-    const int u = base + lane;
-    uint32_t x = u < hi ? a[u] : 0u;
-    if (ghist && x) atomicAdd(&ghist[u], (GH)x);
+  for (int base = lo; base < hi; base += 128) {
+    const int u = base + 4 * lane;
+    uint4 x = make_uint4(0u, 0u, 0u, 0u);
+    if (u < hi) x = *reinterpret_cast<const uint4*>(a + u);
+    if (ghist) {
+      if (x.x) atomicAdd(&ghist[u], (GH)x.x);
+      if (x.y) atomicAdd(&ghist[u + 1], (GH)x.y);
+      if (x.z) atomicAdd(&ghist[u + 2], (GH)x.z);
+      if (x.w) atomicAdd(&ghist[u + 3], (GH)x.w);
+    }
+    x.y += x.x;
+    x.z += x.y;
+    x.w += x.z;
+    uint32_t sum = x.w;
 #pragma unroll
     for (int k = 1; k < 32; k <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, k);
-      if (lane >= k) x += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, sum, k);
+      if (lane >= k) sum += y;
     }
-    x += carry;
-    if (u < hi) a[u] = x;
-    carry = __shfl_sync(0xffffffffu, x, 31);
+    const uint32_t excl = sum - x.w + carry;
+    x.x += excl, x.y += excl, x.z += excl, x.w += excl;
+    if (u < hi) *reinterpret_cast<uint4*>(a + u) = x;
+    carry += __shfl_sync(0xffffffffu, sum, 31);
   }
   if (nw > 1) {
     if (lane == 0) wtot[w] = carry;
@@ -202,43 +221,42 @@ template <bool PEN>
 __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
                                          const uint32_t* vcnt, double* scratch, int gtid, int gsize, int gid_local) {
   const DevTables& tb = P.tb;
-  const int U = tb.U, M = tb.M, maxB = tb.maxB;
+  const int M = tb.M;
   const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
   for (int mp = 0; mp < M * 3; ++mp) {
-    const size_t ob = (size_t)mp * maxB;
     const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
-    const uint32_t* sw = PEN ? SW + (size_t)mp * U : nullptr;
+    const uint32_t* sw = PEN ? SW + (size_t)mp * P.U4 : nullptr;
     double th = 0.0, tm = 0.0, tl = 0.0, eh = 0.0, em = 0.0, el = 0.0;
     long long idle = 0, swc = 0;
     for (int k = k0 + gtid; k < k1; k += gsize) {
-      const int4 sg = __ldg(tb.seg + k);
+      const double2* rec = P.segrec + (size_t)k * 6;
+      const int4 sg = __ldg(reinterpret_cast<const int4*>(rec));
       const uint32_t cnt = C[sg.y] - (sg.x ? C[sg.x - 1] : 0u);
       if (cnt == 0) continue;
-      const size_t o = ob + sg.z;
       const double dc = (double)cnt;
-      const double4 ve = ldg4(P.ven + o);
-      eh = __fma_rn(dc, ve.x, eh);
-      em = __fma_rn(dc, ve.y, em);
-      el = __fma_rn(dc, ve.z, el);
+      const double2 r2 = __ldg(rec + 2), r3 = __ldg(rec + 3);
+      eh = __fma_rn(dc, r2.y, eh);
+      em = __fma_rn(dc, r3.x, em);
+      el = __fma_rn(dc, r3.y, el);
       uint32_t scnt = 0;
       if (PEN) {
         scnt = sw[sg.y] - (sg.x ? sw[sg.x - 1] : 0u);
         swc += scnt;
       }
-      if (ve.w != 0.0) {
+      if (sg.z) {
         idle += cnt;
       } else {
-        const double4 vt = ldg4(P.vthr + o);
+        const double2 r1 = __ldg(rec + 1);
         const double dn = (double)(cnt - scnt);
-        th = __fma_rn(dn, vt.x, th);
-        tm = __fma_rn(dn, vt.y, tm);
-        tl = __fma_rn(dn, vt.z, tl);
+        th = __fma_rn(dn, r1.x, th);
+        tm = __fma_rn(dn, r1.y, tm);
+        tl = __fma_rn(dn, r2.x, tl);
         if (PEN && scnt) {
-          const double4 vp = ldg4(P.vpen + o);
+          const double2 r4 = __ldg(rec + 4), r5 = __ldg(rec + 5);
           const double ds = (double)scnt;
-          th = __fma_rn(ds, vp.x, th);
-          tm = __fma_rn(ds, vp.y, tm);
-          tl = __fma_rn(ds, vp.z, tl);
+          th = __fma_rn(ds, r4.x, th);
+          tm = __fma_rn(ds, r4.y, tm);
+          tl = __fma_rn(ds, r5.x, tl);
         }
       }
     }
@@ -295,18 +313,19 @@ template <bool PEN, typename GH>
 __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* sw,
                                              const uint32_t* vcnt, GH* ghist, double* scratch, int gtid, int gsize,
                                              int gid_local) {
-  const int U = P.tb.U, M = P.tb.M;
-  uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then dd partials
-  group_scan(h, U, ghist, wtot, gtid, gsize, gid_local);
+  const int U4 = P.U4, M = P.tb.M;
+  uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then partial sums
+  group_scan(h, U4, ghist, wtot, gtid, gsize, gid_local);
   if (PEN)
     for (int mp = 0; mp < M * 3; ++mp)
-      group_scan(sw + (size_t)mp * U, U, (uint32_t*)nullptr, wtot, gtid, gsize, gid_local);
+      group_scan(sw + (size_t)mp * U4, U4, (uint32_t*)nullptr, wtot, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
   epilogue<PEN>(P, t, h, sw, vcnt, scratch, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
-  for (int u = gtid; u < U; u += gsize) h[u] = 0u;
+  for (int u = 4 * gtid; u < U4; u += 4 * gsize) *reinterpret_cast<uint4*>(h + u) = make_uint4(0u, 0u, 0u, 0u);
   if (PEN)
-    for (int i = gtid; i < M * 3 * U; i += gsize) sw[i] = 0u;
+    for (int i = 4 * gtid; i < M * 3 * U4; i += 4 * gsize)
+      *reinterpret_cast<uint4*>(sw + i) = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // Exact violation recount of a segment (slow path; only runs if the fast check fired).
@@ -352,48 +371,43 @@ struct Lut32 {
   __device__ __forceinline__ static uint32_t leaf(uint32_t e, uint32_t x, uint32_t mask) {
     return (e + ((x & mask) << 2)) >> 16;  // carries into bit 16 iff the bucket's threshold <= cap
   }
-  __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t x) const {
+  // resolve through redirect sub-tables; ORs the final leaf's "unproven" bit into flags
+  __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t x, uint32_t& flags) const {
     uint32_t s = s1;
     while (e >= kRedirect32) {
       s = e & 31u;
       e = lut[sub0 + ((e >> 5) & 0x7FFu) * kSubFan + ((x >> s) & 15u)];
     }
+    flags |= e;
     return leaf(e, x, ((1u << s) - 1u) & 0x3FFFu);
   }
-  __device__ __forceinline__ uint32_t bin(uint32_t x) const {
+  __device__ __forceinline__ uint32_t bin(uint32_t x, uint32_t& flags) const {
     const uint32_t e = entry(x);
-    return e >= kRedirect32 ? deep(e, x) : leaf(e, x, mask1);
+    if (e >= kRedirect32) return deep(e, x, flags);
+    flags |= e;
+    return leaf(e, x, mask1);
   }
 };
 
-template <int VEC>
-struct VecOut;
-
-// The hot loop over one segment [s0, s1e) of trace t. Returns true if the fast violation
-// check fired (the caller then recounts exactly).
+// The hot loop over one segment [s0, s1e) of trace t. Returns true if a cap met a LUT leaf
+// that is not proven violation-free (the caller then recounts violations exactly).
 template <bool PEN, bool STEP, bool VIO>
-__device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, const uint32_t* s_vio,
-                                                uint32_t* h, uint32_t* sw, const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
+__device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* sw,
+                                                const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
                                                 int gsize) {
-  const int U = P.tb.U, M = P.tb.M;
+  const int U = P.tb.U, U4 = P.U4, M = P.tb.M;
   const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
   const int nvf = n >> 2;
-  bool bad = false;
-
-  auto count = [&](uint32_t b, uint32_t u) {
-    atomicAdd(&h[b], 1u);
-    if (VIO) bad |= u < s_vio[b];  // selected power of every policy must fit under the cap
-                                   // (unsigned: -0.0 and NaN patterns never trip bin 0 / top)
-  };
+  uint32_t flags = 0;  // OR of the leaf entries used: bit 0 = leaf not proven violation-free
   auto switches = [&](uint32_t cb, uint32_t pb) {
     if (cb != pb)
       for (int m = 0; m < M; ++m) {
         const uint64_t xo = s_sig[(size_t)m * U + cb] ^ s_sig[(size_t)m * U + pb];
 #pragma unroll
         for (int p = 0; p < 3; ++p)
-          if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * U + cb], 1u);
+          if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * U4 + cb], 1u);
       }
   };
   auto vec4 = [&](const uint4 raw, int v) {
@@ -403,18 +417,22 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     for (int k = 0; k < 4; ++k) e[k] = L.entry(u[k]);
     uint32_t b[4];
     if (max(max(e[0], e[1]), max(e[2], e[3])) < kRedirect32) {
+      if (VIO) flags |= e[0] | e[1] | e[2] | e[3];
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
     } else {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) b[k] = L.deep(e[k], u[k]);
+      for (int k = 0; k < 4; ++k) b[k] = L.deep(e[k], u[k], flags);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) count(b[k], u[k]);
+    for (int k = 0; k < 4; ++k) atomicAdd(&h[b[k]], 1u);
     const int64_t i0 = s0 + 4 * (int64_t)v;
     if (PEN) {
       uint32_t pb = b[0];  // step 0 is never penalised (sim.py:119)
-      if (i0 > 0) pb = L.bin(__ldg(row + i0 - 1));
+      if (i0 > 0) {
+        uint32_t dummy = 0;
+        pb = L.bin(__ldg(row + i0 - 1), dummy);
+      }
       switches(b[0], pb);
       switches(b[1], b[0]);
       switches(b[2], b[1]);
@@ -444,12 +462,15 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
   for (int i = 4 * nvf + gtid; i < n; i += gsize) {
     const int64_t gi = s0 + i;
     const uint32_t u = __ldg(row + gi);
-    const uint32_t b = L.bin(u);
-    count(b, u);
-    if (PEN) switches(b, gi > 0 ? L.bin(__ldg(row + gi - 1)) : b);
+    const uint32_t b = L.bin(u, flags);
+    atomicAdd(&h[b], 1u);
+    if (PEN) {
+      uint32_t dummy = 0;
+      switches(b, gi > 0 ? L.bin(__ldg(row + gi - 1), dummy) : b);
+    }
     if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
   }
-  return bad;
+  return VIO && (flags & 1u);
 }
 
 template <bool PEN, bool STEP, bool VIO>
@@ -474,7 +495,7 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint3
         for (int m = 0; m < M; ++m) {
           const uint64_t xo = s_sig[(size_t)m * U + b] ^ s_sig[(size_t)m * U + pb];
           for (int p = 0; p < 3; ++p)
-            if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * U + b], 1u);
+            if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * P.U4 + b], 1u);
         }
     }
     if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
@@ -505,16 +526,10 @@ __global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ Ev
   // ---- N1: stage the tables into shared memory once per CTA ----
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
   for (int i = threadIdx.x; i < tb.n_lut; i += blockDim.x) s_lut[i] = __ldg(tb.lv.lut + i);
-  // violation floors: lowest admissible cap bits per union bin (u32 for fp32 tables)
+  // fp64 tables: violation floors per union bin (fp32 tables carry the proof in the LUT leaves)
   uint64_t* s_vio = reinterpret_cast<uint64_t*>(smem + P.off_vio);
-  uint32_t* s_vio32 = reinterpret_cast<uint32_t*>(smem + P.off_vio);
-  if (VIO)
-    for (int i = threadIdx.x; i < U; i += blockDim.x) {
-      if (F32)
-        s_vio32[i] = (uint32_t)__ldg(tb.vio + i);
-      else
-        s_vio[i] = __ldg(tb.vio + i);
-    }
+  if (!F32 && VIO)
+    for (int i = threadIdx.x; i < U; i += blockDim.x) s_vio[i] = __ldg(tb.vio + i);
   uint64_t* s_sig = reinterpret_cast<uint64_t*>(smem + P.off_sig);
   if (PEN)
     for (int i = threadIdx.x; i < M * U; i += blockDim.x) s_sig[i] = __ldg(tb.sig + i);
@@ -537,9 +552,10 @@ __global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ Ev
   uint32_t* sw = reinterpret_cast<uint32_t*>(gbase + P.off_g_sw);
   uint32_t* vcnt = reinterpret_cast<uint32_t*>(gbase + P.off_g_vio);
   double* scratch = reinterpret_cast<double*>(gbase + P.off_g_scr);
-  for (int u = gtid; u < U; u += gsize) h[u] = 0u;
+  const int U4 = P.U4;
+  for (int u = gtid; u < U4; u += gsize) h[u] = 0u;
   if (PEN)
-    for (int i = gtid; i < M * 3 * U; i += gsize) sw[i] = 0u;
+    for (int i = gtid; i < M * 3 * U4; i += gsize) sw[i] = 0u;
   if (gtid < M * 3) vcnt[gtid] = 0u;
   if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag
   __syncthreads();
@@ -560,7 +576,7 @@ __global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ Ev
     const int64_t s1e = min(P.S, s0 + P.seg_len);
     bool bad;
     if constexpr (F32)
-      bad = run_segment_f32<PEN, STEP, VIO>(P, L, s_vio32, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+      bad = run_segment_f32<PEN, STEP, VIO>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     else
       bad = run_segment_f64<PEN, STEP, VIO>(P, s_lut, s_vio, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     if (VIO && bad) atomicOr(&vcnt[M * 3], 1u);
@@ -592,14 +608,14 @@ __global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ Ev
       for (int u = gtid; u < U; u += gsize) {
         const uint32_t c = h[u];
         if (c) {
-          atomicAdd(&P.part_hist[t * U + u], c);
+          atomicAdd(&P.part_hist[t * U4 + u], c);
           h[u] = 0u;
           if (PEN)
             for (int mp = 0; mp < M * 3; ++mp) {
-              const uint32_t s = sw[(size_t)mp * U + u];
+              const uint32_t s = sw[(size_t)mp * U4 + u];
               if (s) {
-                atomicAdd(&P.part_sw[(t * M * 3 + mp) * U + u], s);
-                sw[(size_t)mp * U + u] = 0u;
+                atomicAdd(&P.part_sw[(t * M * 3 + mp) * U4 + u], s);
+                sw[(size_t)mp * U4 + u] = 0u;
               }
             }
         }
@@ -624,9 +640,9 @@ template <bool PEN>
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EvalParams P) {
   __shared__ double scratch[8 * 8];
   const int64_t t = blockIdx.x;
-  const int U = P.tb.U, M = P.tb.M;
-  uint32_t* h = P.part_hist + t * U;
-  uint32_t* sw = PEN ? P.part_sw + t * (int64_t)M * 3 * U : nullptr;
+  const int U4 = P.U4, M = P.tb.M;
+  uint32_t* h = P.part_hist + t * U4;
+  uint32_t* sw = PEN ? P.part_sw + t * (int64_t)M * 3 * U4 : nullptr;
   const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
   finish_trace<PEN>(P, t, h, sw, vc, P.hist, scratch, threadIdx.x, blockDim.x, 0);
 }
@@ -686,15 +702,16 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int nsm = sm_count(dev);
   const size_t lut_bytes = a16((size_t)t.lut.size() * 4);
-  const size_t vio_bytes = vio ? a16((size_t)U * (f32 ? 4 : 8)) : 0;
+  const size_t vio_bytes = (vio && !f32) ? a16((size_t)U * 8) : 0;
+  const int U4 = (U + 3) & ~3;
   const size_t sig_bytes = pen ? a16((size_t)M * U * 8) : 0;
   const size_t gh_bytes = a->hist ? a16((size_t)U * 4 + 4) : 0;
   const size_t fixed = lut_bytes + vio_bytes + sig_bytes + gh_bytes;
   const int hs = 1;
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
-    size_t gb = a16((size_t)U * 4 * hs);
+    size_t gb = a16((size_t)U4 * 4 * hs);
     *off_sw = gb;
-    gb += pen ? a16((size_t)M * 3 * U * 4) : 0;
+    gb += pen ? a16((size_t)M * 3 * U4 * 4) : 0;
     *off_v = gb;
     gb += a16((size_t)(M * 3 + 1) * 4);
     *off_scr = gb;
@@ -746,9 +763,9 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   pl.seg_len = seg_len;
   pl.ctas = (int)std::max<int64_t>(
       1, std::min<int64_t>((int64_t)nsm * b_per_sm, (a->n_traces * nseg + pl.gpc - 1) / pl.gpc));
-  pl.ws_prep = a16((size_t)M * 3 * t.maxB * 32) * 3;
+  pl.ws_prep = a16((size_t)(t.seg.size() / 4) * 96);
   pl.ws_split = nseg > 1 ? (size_t)a->n_traces *
-                               ((size_t)U + (pen ? (size_t)M * 3 * U : 0) + (size_t)M * 3) * sizeof(uint32_t)
+                               ((size_t)U4 + (pen ? (size_t)M * 3 * U4 : 0) + (size_t)M * 3) * sizeof(uint32_t)
                          : 0;
 
   EvalParams& P = pl.P;
@@ -773,6 +790,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.wpg = pl.wpg;
   P.gpc = pl.gpc;
   P.hstride = hs;
+  P.U4 = U4;
   P.off_vio = (int32_t)lut_bytes;
   P.off_sig = (int32_t)(lut_bytes + vio_bytes);
   P.off_ghist = (int32_t)(lut_bytes + vio_bytes + sig_bytes);
@@ -809,24 +827,21 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   if (a->workspace == nullptr || a->workspace_bytes < need)
     return "workspace too small: need " + std::to_string(need) + " bytes (cs_eval_workspace_size)";
   unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace);
-  const size_t nv = (size_t)t.M * 3 * t.maxB;
-  double4* vthr = reinterpret_cast<double4*>(ws);
-  double4* vpen = reinterpret_cast<double4*>(ws + a16(nv * 32));
-  double4* ven = reinterpret_cast<double4*>(ws + 2 * a16(nv * 32));
-  P.vthr = vthr, P.vpen = vpen, P.ven = ven;
+  double2* segrec = reinterpret_cast<double2*>(ws);
+  P.segrec = segrec;
   // bits per exact level: counts up to S must keep count x hi below 2^53 quanta
   int L = 26;
   while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
   int launches = 0;
-  prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, vthr, vpen, ven);
+  prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, segrec);
   CS_CUDA_TRY(cudaGetLastError());
   ++launches;
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
   if (pl.nseg > 1) {
     uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);
     P.part_hist = w;
-    P.part_sw = w + (size_t)a->n_traces * t.U;
-    P.part_vio = P.part_sw + (pen ? (size_t)a->n_traces * t.M * 3 * t.U : 0);
+    P.part_sw = w + (size_t)a->n_traces * P.U4;
+    P.part_vio = P.part_sw + (pen ? (size_t)a->n_traces * t.M * 3 * P.U4 : 0);
     CS_CUDA_TRY(cudaMemsetAsync(w, 0, pl.ws_split, st));
   }
   void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio);

@@ -72,10 +72,24 @@ bool in_regime(int p, const Entry& e, int32_t bmtl, int32_t mbs) {
 struct LutBuilder {
   const std::vector<uint64_t>& T;
   bool f32;
+  const std::vector<uint64_t>* vio = nullptr;  // fp32: violation floors per union bin
   std::vector<uint32_t> sub;  // sub-table entries (appended after level 1)
   uint32_t n_sub = 0;
+  uint32_t unsafe = 0;        // fp32 leaves whose selections are not proven to fit their caps
 
-  LutBuilder(const std::vector<uint64_t>& t, bool is_f32) : T(t), f32(is_f32) {}
+  LutBuilder(const std::vector<uint64_t>& t, bool is_f32, const std::vector<uint64_t>* v = nullptr)
+      : T(t), f32(is_f32), vio(v) {}
+
+  // Bit 0 of an fp32 leaf (free: K is a multiple of 4) flags a leaf for which some cap of its
+  // range could select a config drawing more than the cap. Proof per leaf: every cap of the
+  // bucket is >= `start` and maps to bin `b0`; caps >= `t1` (the bucket's threshold) map to b0+1.
+  uint32_t flag(uint64_t start, uint32_t b0, bool has_t1, uint64_t t1) {
+    if (!vio) return 0u;
+    bool ok = (*vio)[b0] <= start;
+    if (has_t1) ok = ok && (*vio)[b0 + 1] <= t1;
+    if (!ok) ++unsafe;
+    return ok ? 0u : 1u;
+  }
 
   uint32_t lb(uint64_t v) const { return (uint32_t)(std::lower_bound(T.begin(), T.end(), v) - T.begin()); }
 
@@ -87,11 +101,11 @@ struct LutBuilder {
     uint32_t stop = (s >= 63) ? (uint32_t)T.size() : lb(end);
     uint32_t n = stop - base;
     if (f32) {
-      if (n == 0) return base << 16;
+      if (n == 0) return (base << 16) | flag(start, base, false, 0);
       if (n == 1 && s <= 14) {
         const uint32_t tl = (uint32_t)(T[base] - start);
-        if (tl == 0) return (base + 1) << 16;  // threshold on the bucket start: every cap is above
-        return (base << 16) | ((0x4000u - tl) << 2);
+        if (tl == 0) return ((base + 1) << 16) | flag(start, base + 1, false, 0);  // threshold on the start
+        return (base << 16) | ((0x4000u - tl) << 2) | flag(start, base, true, T[base]);
       }
     } else {
       if (n == 0) return base << 16;
@@ -108,7 +122,7 @@ struct LutBuilder {
       } else {
         uint64_t v = (start & ~15ull) | i;
         if (v >= start && v < end) ent = make(v, 0);
-        else ent = lb(v) << 16;  // unreachable slot
+        else ent = lb(v) << 16;  // unreachable slot (never indexed by a cap of this bucket)
       }
       sub[off + i] = ent;
     }
@@ -307,7 +321,7 @@ std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap
     const uint32_t s = best_s;
     uint64_t kb, nb;
     if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
-    LutBuilder lbld(T, f32);
+    LutBuilder lbld(T, f32, f32 ? &t.vio : nullptr);
     t.kbase = kb;
     std::vector<uint32_t> level1(nb);
     for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
@@ -317,6 +331,7 @@ std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap
     t.shift1 = s;
     t.n_level1 = (uint32_t)nb;
     t.n_sub = lbld.n_sub;
+    t.n_unsafe = lbld.unsafe;
     t.lut = std::move(level1);
     t.lut.insert(t.lut.end(), lbld.sub.begin(), lbld.sub.end());
   }

@@ -107,3 +107,16 @@ def test_negative_zero_and_bad_grids():
     for dt in ("f32", "f64"):
         t = Tables.stage([g], dt)
         assert list(t.lookup_host(np.array([-0.0, 0.0, 99.9, 100.0, 1e9]))) == [0, 0, 0, 1, 1]
+
+
+def test_lut_leaves_proven_violation_free():
+    """Every fp32 LUT leaf of every golden grid is proven (at staging) to select only configs
+    whose power fits all caps the leaf serves — the basis of the kernel's per-step check."""
+    doc = golden("policy_golden.json")
+    for case in doc["cases"]:
+        grid = grid_from_doc(case["grid"])
+        t = Tables.stage([grid], "f32", batching_mtl=case["batching_mtl"], multi_tenant_bs=case["multi_tenant_bs"])
+        assert t.info.lut_unsafe_leaves == 0, case["name"]
+        assert t.info.n_segments >= 3
+    g = synthesize_grid(SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
+    assert Tables.stage([g], "f32").info.lut_unsafe_leaves == 0
