@@ -211,98 +211,140 @@ __device__ __forceinline__ void group_scan(uint32_t* a, int U4, GH* ghist, uint3
   }
 }
 
+// Transposed butterfly reduction of 6 per-lane doubles across a warp (reduce-scatter):
+// 3+2+1+1+1 = 8 exchanges instead of 6 x 5. Afterwards lane kLaneOf6[j] holds the warp total
+// of value j.
+__constant__ int kLaneOf6[6] = {0, 4, 8, 16, 20, 24};
+
+__device__ __forceinline__ double xreduce6(const double (&v)[6], int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double a[3], b[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double keep = b4 ? v[3 + i] : v[i], send = b4 ? v[i] : v[3 + i];
+    a[i] = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 16));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double lo = a[i], hi = i < 1 ? a[2 + i] : 0.0;
+    const double keep = b3 ? hi : lo, send = b3 ? lo : hi;
+    b[i] = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 8));
+  }
+  const double keep = b2 ? b[1] : b[0], send = b2 ? b[0] : b[1];
+  double c = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 4));
+  c = __dadd_rn(c, __shfl_xor_sync(FULL, c, 2));
+  return __dadd_rn(c, __shfl_xor_sync(FULL, c, 1));
+}
+
 // Per-trace epilogue: every (grid, policy) aggregate of _aggregate (sim.py:104-127) from the
 // group's prefix-summed histogram. Union bins with the same selected config form a segment
-// (staged in tb.seg); a segment's step count is C[hi] - C[lo-1], so each thread handles whole
-// segments: sum += count x value in double-double (exactly rounded like math.fsum).
-//   C[u]               prefix-summed step counts (scanned in place)
-//   SW[(m*3+p)*U + u]  prefix-summed switched-step counts (PEN)
+// (staged in tb.seg); a segment's step count is C[hi] - C[lo-1]. Threads stride over a
+// policy's segments accumulating count x {hi, mid, lo} per value (hi and mid sums are exact),
+// then one transposed warp reduction per policy; lanes 0..2 finalize one policy each.
+//   C[u]                prefix-summed step counts (scanned in place)
+//   SW[(m*3+p)*U4 + u]  prefix-summed switched-step counts (PEN)
 template <bool PEN>
 __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
                                          const uint32_t* vcnt, double* scratch, int gtid, int gsize, int gid_local) {
   const DevTables& tb = P.tb;
   const int M = tb.M;
   const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
-  for (int mp = 0; mp < M * 3; ++mp) {
-    const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
-    const uint32_t* sw = PEN ? SW + (size_t)mp * P.U4 : nullptr;
-    double th = 0.0, tm = 0.0, tl = 0.0, eh = 0.0, em = 0.0, el = 0.0;
-    long long idle = 0, swc = 0;
-    for (int k = k0 + gtid; k < k1; k += gsize) {
-      const double2* rec = P.segrec + (size_t)k * 6;
-      const int4 sg = __ldg(reinterpret_cast<const int4*>(rec));
-      const uint32_t cnt = C[sg.y] - (sg.x ? C[sg.x - 1] : 0u);
-      if (cnt == 0) continue;
-      const double dc = (double)cnt;
-      const double2 r2 = __ldg(rec + 2), r3 = __ldg(rec + 3);
-      eh = __fma_rn(dc, r2.y, eh);
-      em = __fma_rn(dc, r3.x, em);
-      el = __fma_rn(dc, r3.y, el);
-      uint32_t scnt = 0;
-      if (PEN) {
-        scnt = sw[sg.y] - (sg.x ? sw[sg.x - 1] : 0u);
-        swc += scnt;
-      }
-      if (sg.z) {
-        idle += cnt;
-      } else {
-        const double2 r1 = __ldg(rec + 1);
-        const double dn = (double)(cnt - scnt);
-        th = __fma_rn(dn, r1.x, th);
-        tm = __fma_rn(dn, r1.y, tm);
-        tl = __fma_rn(dn, r2.x, tl);
-        if (PEN && scnt) {
-          const double2 r4 = __ldg(rec + 4), r5 = __ldg(rec + 5);
-          const double ds = (double)scnt;
-          th = __fma_rn(ds, r4.x, th);
-          tm = __fma_rn(ds, r4.y, tm);
-          tl = __fma_rn(ds, r5.x, tl);
-        }
-      }
-    }
-    // hi / mid partial sums are exact multiples of their quanta: plain adds stay exact
+  for (int m = 0; m < M; ++m) {
+    double mine[3];
+    uint32_t ired[6];
 #pragma unroll
-    for (int k = 16; k >= 1; k >>= 1) {
-      th = __dadd_rn(th, __shfl_xor_sync(0xffffffffu, th, k));
-      tm = __dadd_rn(tm, __shfl_xor_sync(0xffffffffu, tm, k));
-      tl = __dadd_rn(tl, __shfl_xor_sync(0xffffffffu, tl, k));
-      eh = __dadd_rn(eh, __shfl_xor_sync(0xffffffffu, eh, k));
-      em = __dadd_rn(em, __shfl_xor_sync(0xffffffffu, em, k));
-      el = __dadd_rn(el, __shfl_xor_sync(0xffffffffu, el, k));
-      idle += __shfl_xor_sync(0xffffffffu, idle, k);
-      swc += __shfl_xor_sync(0xffffffffu, swc, k);
+    for (int p = 0; p < 3; ++p) {
+      const int mp = 3 * m + p;
+      const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
+      const uint32_t* sw = PEN ? SW + (size_t)mp * P.U4 : nullptr;
+      double a[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // thr hi, mid, lo, energy hi, mid, lo
+      uint32_t idle = 0, swc = 0;
+      for (int k = k0 + gtid; k < k1; k += gsize) {
+        const double2* rec = P.segrec + (size_t)k * 6;
+        const int4 sg = __ldg(reinterpret_cast<const int4*>(rec));
+        const uint32_t cnt = C[sg.y] - (sg.x ? C[sg.x - 1] : 0u);
+        if (cnt == 0) continue;
+        const double dc = (double)cnt;
+        const double2 r2 = __ldg(rec + 2), r3 = __ldg(rec + 3);
+        a[3] = __fma_rn(dc, r2.y, a[3]);
+        a[4] = __fma_rn(dc, r3.x, a[4]);
+        a[5] = __fma_rn(dc, r3.y, a[5]);
+        uint32_t scnt = 0;
+        if (PEN) {
+          scnt = sw[sg.y] - (sg.x ? sw[sg.x - 1] : 0u);
+          swc += scnt;
+        }
+        if (sg.z) {
+          idle += cnt;
+        } else {
+          const double2 r1 = __ldg(rec + 1);
+          const double dn = (double)(cnt - scnt);
+          a[0] = __fma_rn(dn, r1.x, a[0]);
+          a[1] = __fma_rn(dn, r1.y, a[1]);
+          a[2] = __fma_rn(dn, r2.x, a[2]);
+          if (PEN && scnt) {
+            const double2 r4 = __ldg(rec + 4), r5 = __ldg(rec + 5);
+            const double ds = (double)scnt;
+            a[0] = __fma_rn(ds, r4.x, a[0]);
+            a[1] = __fma_rn(ds, r4.y, a[1]);
+            a[2] = __fma_rn(ds, r5.x, a[2]);
+          }
+        }
+      }
+      mine[p] = xreduce6(a, lane);
+      ired[p] = __reduce_add_sync(0xffffffffu, idle);
+      ired[3 + p] = PEN ? __reduce_add_sync(0xffffffffu, swc) : 0u;
     }
-    if (nw > 1) {
-      if (lane == 0) {
-        double* d = scratch + wig * 8;
-        d[0] = th, d[1] = tm, d[2] = tl, d[3] = eh, d[4] = em, d[5] = el;
-        d[6] = __longlong_as_double(idle), d[7] = __longlong_as_double(swc);
+    if (nw > 1) {  // combine the warps of the group through shared scratch (18 + 6 words / warp)
+      double* d = scratch + wig * 24;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          if (lane == kLaneOf6[c]) d[6 * p + c] = mine[p];
+      if (lane == 0)
+        for (int j = 0; j < 6; ++j) d[18 + j] = __longlong_as_double((long long)ired[j]);
+      group_sync(gid_local, gsize);
+      if (wig == 0) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int c = 0; c < 6; ++c)
+            if (lane == kLaneOf6[c])
+              for (int w = 1; w < nw; ++w) mine[p] = __dadd_rn(mine[p], scratch[w * 24 + 6 * p + c]);
+        for (int w = 1; w < nw; ++w)
+          for (int j = 0; j < 6; ++j) ired[j] += (uint32_t)__double_as_longlong(scratch[w * 24 + 18 + j]);
       }
       group_sync(gid_local, gsize);
-      if (gtid == 0)
-        for (int w = 1; w < nw; ++w) {
-          const double* d = scratch + w * 8;
-          th = __dadd_rn(th, d[0]), tm = __dadd_rn(tm, d[1]), tl = __dadd_rn(tl, d[2]);
-          eh = __dadd_rn(eh, d[3]), em = __dadd_rn(em, d[4]), el = __dadd_rn(el, d[5]);
-          idle += __double_as_longlong(d[6]);
-          swc += __double_as_longlong(d[7]);
-        }
-      group_sync(gid_local, gsize);
     }
-    if (gtid == 0 && P.agg) {
-      dd tsum{th, 0.0}, esum{eh, 0.0};
-      dd_add2(tsum, tm, 0.0);
-      dd_add2(tsum, tl, 0.0);
-      dd_add2(esum, em, 0.0);
-      dd_add2(esum, el, 0.0);
-      cs_agg a;
-      a.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
-      a.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
-      a.idle_steps = idle;
-      a.switches = swc;
-      a.violations = vcnt ? vcnt[mp] : 0;
-      a.num_steps = P.S;
-      P.agg[t * M * 3 + mp] = a;
+    if (wig == 0) {
+      // lane q (< 3) gathers policy q's six sums and writes its aggregate
+      double part[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        const double x0 = __shfl_sync(0xffffffffu, mine[0], kLaneOf6[c]);
+        const double x1 = __shfl_sync(0xffffffffu, mine[1], kLaneOf6[c]);
+        const double x2 = __shfl_sync(0xffffffffu, mine[2], kLaneOf6[c]);
+        part[c] = lane == 0 ? x0 : (lane == 1 ? x1 : x2);
+      }
+      if (lane < 3 && P.agg) {
+        dd tsum{part[0], 0.0}, esum{part[3], 0.0};
+        dd_add2(tsum, part[1], 0.0);
+        dd_add2(tsum, part[2], 0.0);
+        dd_add2(esum, part[4], 0.0);
+        dd_add2(esum, part[5], 0.0);
+        const uint32_t id = lane == 0 ? ired[0] : (lane == 1 ? ired[1] : ired[2]);
+        const uint32_t sc = lane == 0 ? ired[3] : (lane == 1 ? ired[4] : ired[5]);
+        cs_agg a;
+        a.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
+        a.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
+        a.idle_steps = id;
+        a.switches = sc;
+        a.violations = vcnt ? vcnt[3 * m + lane] : 0;
+        a.num_steps = P.S;
+        P.agg[t * M * 3 + 3 * m + lane] = a;
+      }
     }
   }
 }
@@ -638,7 +680,7 @@ __global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ Ev
 
 template <bool PEN>
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EvalParams P) {
-  __shared__ double scratch[8 * 8];
+  __shared__ double scratch[8 * 24];
   const int64_t t = blockIdx.x;
   const int U4 = P.U4, M = P.tb.M;
   uint32_t* h = P.part_hist + t * U4;
@@ -715,7 +757,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     *off_v = gb;
     gb += a16((size_t)(M * 3 + 1) * 4);
     *off_scr = gb;
-    gb += (size_t)wpg * 8 * 8;
+    gb += (size_t)wpg * 24 * 8;
     return a16(gb);
   };
   // candidates: most resident warps per SM first, then the smallest worker group
