@@ -284,12 +284,14 @@ def main() -> None:
     bytes_per_launch = T * S * 4 + T * M * 3 * 48 + tables.n_union_bins * 8
     achieved_gbs = bytes_per_launch / (kernel_ms / 1e3) / 1e9
     peak, peak_src = peaks()
+    # DRAM bytes per launch from the committed ncu --set full capture of this workload
+    # (tools/ncu_summary.py --traffic-key), scaled from bytes per timestep to this launch
     traffic = None
     tpath = ROOT / "profiles" / "ncu_traffic.json"
     if tpath.exists():
-        tdoc = json.loads(tpath.read_text()).get(f"{args.config}:{cfg['kind']}:{T}")
+        tdoc = json.loads(tpath.read_text()).get(f"{args.config}:{cfg['kind']}")
         if tdoc:
-            traffic = tdoc.get("dram_bytes_per_launch")
+            traffic = tdoc["dram_bytes_per_timestep"] * T * S
 
     out = None
     if rank == 0:

@@ -8,11 +8,12 @@ never silently runs a CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libcapsim_b200.so"
+LIB_PATH = Path(os.environ.get("CAPSIM_B200_LIB") or Path(__file__).resolve().parent / "_lib" / "libcapsim_b200.so")
 
 CS_OK = 0
 CS_E_INVALID = -1

@@ -51,32 +51,36 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines: tuple = ()) -> Path:
+    """Compile the library (``out``/``defines`` build experiment variants next to it)."""
+    lib = out or LIB
+    if not force and out is None and not stale():
         return LIB
     LIBDIR.mkdir(exist_ok=True)
     objs = []
     log = []
     for src in SOURCES:
-        obj = LIBDIR / (src + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+        obj = LIBDIR / (lib.stem + "." + src + ".o")
+        dflags = [f"-D{d}" for d in defines]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *dflags, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
         if src.endswith(".cpp"):
-            cmd = [nvcc(), "-x", "cu", *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+            cmd = [nvcc(), "-x", "cu", *ARCH, *NVCC_FLAGS, *dflags, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o",
+                   str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart=static", "-o", str(tmp), *objs, "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    (LIBDIR / "ptxas.log").write_text("\n".join(log))
+    os.replace(tmp, lib)
+    (LIBDIR / (lib.stem + ".ptxas.log")).write_text("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

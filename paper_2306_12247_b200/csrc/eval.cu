@@ -105,21 +105,19 @@ __device__ __forceinline__ void group_sync(int gid_local, int gsize) {
 
 // prep: per selection segment, the fp64 values of this launch computed exactly like the
 // reference per step (sim.py:111, 119-122): thr, thr * (1 - pf), (power or idle) * step / 3600.
-// Each value v is split as v = hi + mid + lo with hi a multiple of Q = 2^(E+1-L) (E = exponent
-// of the (grid, policy) table's largest value) and mid a multiple of Q*2^-L: for any count
-// c < 2^(53-L), c*hi and c*mid are exact and so are their running sums over a trace, so the
-// epilogue needs three FMAs per value instead of a double-double accumulation.
-// One block per (grid, policy).
-__device__ __forceinline__ void split3(double v, int eq, int L, double* out) {
+// Each value v is split as v = hi + lo with hi = floor(v / Q) * Q, Q = 2^(E+1-L) (E: exponent of
+// the (grid, policy) table's largest value, L = 53 - bits(S)): for any count c <= S, c * hi and
+// the running sum of such products over a trace are EXACT (integers times Q below 2^53 Q); the
+// small lo parts are summed in plain fp64 (error ~2^-(53+L) of the total), so the final
+// hi + lo rounds to the exactly rounded sum the reference's math.fsum returns.
+// Record per segment (4 x 16 B): {u_lo, u_hi, idle, -}, {thr hi, lo}, {energy hi, lo},
+// {penalised thr hi, lo}. One block per (grid, policy).
+__device__ __forceinline__ double2 split2(double v, int eq) {
   const double hi = ldexp(floor(ldexp(v, -eq)), eq);  // floor(v / Q) * Q, exact
-  const double r = v - hi;
-  const double mid = ldexp(floor(ldexp(r, L - eq)), eq - L);
-  out[0] = hi;
-  out[1] = mid;
-  out[2] = r - mid;
+  return make_double2(hi, v - hi);
 }
 
-__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, double2* segrec) {
+__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, double2* segrec) {  // L: see split2
   __shared__ double red[2][256];
   const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
   const size_t ob = (size_t)mp * B;
@@ -150,19 +148,12 @@ __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, 
     const int4 sg = tb.seg[k];
     const size_t i = ob + sg.z;
     const bool idle = tb.sel[i] < 0;
-    double v[12];
-    split3(idle ? 0.0 : tb.sthr[i], et, L, v + 0);
-    split3(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee, L, v + 3);
-    split3(idle ? 0.0 : __dmul_rn(tb.sthr[i], omp), et, L, v + 6);
-    v[9] = 0.0;
-    double2* out = segrec + (size_t)k * 6;
+    double2* out = segrec + (size_t)k * 4;
     int4 head = make_int4(sg.x, sg.y, idle ? 1 : 0, 0);
     out[0] = *reinterpret_cast<const double2*>(&head);
-    out[1] = make_double2(v[0], v[1]);   // thr hi, mid
-    out[2] = make_double2(v[2], v[3]);   // thr lo, en hi
-    out[3] = make_double2(v[4], v[5]);   // en mid, lo
-    out[4] = make_double2(v[6], v[7]);   // pen hi, mid
-    out[5] = make_double2(v[8], v[9]);   // pen lo
+    out[1] = split2(idle ? 0.0 : tb.sthr[i], et);
+    out[2] = split2(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee);
+    out[3] = split2(idle ? 0.0 : __dmul_rn(tb.sthr[i], omp), et);
   }
 }
 
@@ -211,28 +202,23 @@ __device__ __forceinline__ void group_scan(uint32_t* a, int U4, GH* ghist, uint3
   }
 }
 
-// Transposed butterfly reduction of 6 per-lane doubles across a warp (reduce-scatter):
-// 3+2+1+1+1 = 8 exchanges instead of 6 x 5. Afterwards lane kLaneOf6[j] holds the warp total
+// Transposed butterfly reduction of 4 per-lane doubles across a warp (reduce-scatter):
+// 2+1+1+1+1 = 6 exchanges instead of 4 x 5. Afterwards lane kLaneOf4[j] holds the warp total
 // of value j.
-__constant__ int kLaneOf6[6] = {0, 4, 8, 16, 20, 24};
+__constant__ int kLaneOf4[4] = {0, 8, 16, 24};
 
-__device__ __forceinline__ double xreduce6(const double (&v)[6], int lane) {
+__device__ __forceinline__ double xreduce4(const double (&v)[4], int lane) {
   const unsigned FULL = 0xffffffffu;
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-  double a[3], b[2];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const double keep = b4 ? v[3 + i] : v[i], send = b4 ? v[i] : v[3 + i];
-    a[i] = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 16));
-  }
+  const bool b4 = lane & 16, b3 = lane & 8;
+  double a[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const double lo = a[i], hi = i < 1 ? a[2 + i] : 0.0;
-    const double keep = b3 ? hi : lo, send = b3 ? lo : hi;
-    b[i] = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 8));
+    const double keep = b4 ? v[2 + i] : v[i], send = b4 ? v[i] : v[2 + i];
+    a[i] = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 16));
   }
-  const double keep = b2 ? b[1] : b[0], send = b2 ? b[0] : b[1];
-  double c = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 4));
+  const double keep = b3 ? a[1] : a[0], send = b3 ? a[0] : a[1];
+  double c = __dadd_rn(keep, __shfl_xor_sync(FULL, send, 8));
+  c = __dadd_rn(c, __shfl_xor_sync(FULL, c, 4));
   c = __dadd_rn(c, __shfl_xor_sync(FULL, c, 2));
   return __dadd_rn(c, __shfl_xor_sync(FULL, c, 1));
 }
@@ -258,18 +244,17 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
       const int mp = 3 * m + p;
       const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
       const uint32_t* sw = PEN ? SW + (size_t)mp * P.U4 : nullptr;
-      double a[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // thr hi, mid, lo, energy hi, mid, lo
+      double a[4] = {0.0, 0.0, 0.0, 0.0};  // thr hi, lo, energy hi, lo
       uint32_t idle = 0, swc = 0;
       for (int k = k0 + gtid; k < k1; k += gsize) {
-        const double2* rec = P.segrec + (size_t)k * 6;
+        const double2* rec = P.segrec + (size_t)k * 4;
         const int4 sg = __ldg(reinterpret_cast<const int4*>(rec));
         const uint32_t cnt = C[sg.y] - (sg.x ? C[sg.x - 1] : 0u);
         if (cnt == 0) continue;
+        const double2 ve = __ldg(rec + 2);
         const double dc = (double)cnt;
-        const double2 r2 = __ldg(rec + 2), r3 = __ldg(rec + 3);
-        a[3] = __fma_rn(dc, r2.y, a[3]);
-        a[4] = __fma_rn(dc, r3.x, a[4]);
-        a[5] = __fma_rn(dc, r3.y, a[5]);
+        a[2] = __fma_rn(dc, ve.x, a[2]);
+        a[3] = __fma_rn(dc, ve.y, a[3]);
         uint32_t scnt = 0;
         if (PEN) {
           scnt = sw[sg.y] - (sg.x ? sw[sg.x - 1] : 0u);
@@ -278,21 +263,19 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
         if (sg.z) {
           idle += cnt;
         } else {
-          const double2 r1 = __ldg(rec + 1);
+          const double2 vt = __ldg(rec + 1);
           const double dn = (double)(cnt - scnt);
-          a[0] = __fma_rn(dn, r1.x, a[0]);
-          a[1] = __fma_rn(dn, r1.y, a[1]);
-          a[2] = __fma_rn(dn, r2.x, a[2]);
+          a[0] = __fma_rn(dn, vt.x, a[0]);
+          a[1] = __fma_rn(dn, vt.y, a[1]);
           if (PEN && scnt) {
-            const double2 r4 = __ldg(rec + 4), r5 = __ldg(rec + 5);
+            const double2 vp = __ldg(rec + 3);
             const double ds = (double)scnt;
-            a[0] = __fma_rn(ds, r4.x, a[0]);
-            a[1] = __fma_rn(ds, r4.y, a[1]);
-            a[2] = __fma_rn(ds, r5.x, a[2]);
+            a[0] = __fma_rn(ds, vp.x, a[0]);
+            a[1] = __fma_rn(ds, vp.y, a[1]);
           }
         }
       }
-      mine[p] = xreduce6(a, lane);
+      mine[p] = xreduce4(a, lane);
       ired[p] = __reduce_add_sync(0xffffffffu, idle);
       ired[3 + p] = PEN ? __reduce_add_sync(0xffffffffu, swc) : 0u;
     }
@@ -301,39 +284,37 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
-        for (int c = 0; c < 6; ++c)
-          if (lane == kLaneOf6[c]) d[6 * p + c] = mine[p];
+        for (int c = 0; c < 4; ++c)
+          if (lane == kLaneOf4[c]) d[4 * p + c] = mine[p];
       if (lane == 0)
-        for (int j = 0; j < 6; ++j) d[18 + j] = __longlong_as_double((long long)ired[j]);
+        for (int j = 0; j < 6; ++j) d[12 + j] = __longlong_as_double((long long)ired[j]);
       group_sync(gid_local, gsize);
       if (wig == 0) {
 #pragma unroll
         for (int p = 0; p < 3; ++p)
 #pragma unroll
-          for (int c = 0; c < 6; ++c)
-            if (lane == kLaneOf6[c])
-              for (int w = 1; w < nw; ++w) mine[p] = __dadd_rn(mine[p], scratch[w * 24 + 6 * p + c]);
+          for (int c = 0; c < 4; ++c)
+            if (lane == kLaneOf4[c])
+              for (int w = 1; w < nw; ++w) mine[p] = __dadd_rn(mine[p], scratch[w * 24 + 4 * p + c]);
         for (int w = 1; w < nw; ++w)
-          for (int j = 0; j < 6; ++j) ired[j] += (uint32_t)__double_as_longlong(scratch[w * 24 + 18 + j]);
+          for (int j = 0; j < 6; ++j) ired[j] += (uint32_t)__double_as_longlong(scratch[w * 24 + 12 + j]);
       }
       group_sync(gid_local, gsize);
     }
     if (wig == 0) {
       // lane q (< 3) gathers policy q's six sums and writes its aggregate
-      double part[6];
+      double part[4];
 #pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        const double x0 = __shfl_sync(0xffffffffu, mine[0], kLaneOf6[c]);
-        const double x1 = __shfl_sync(0xffffffffu, mine[1], kLaneOf6[c]);
-        const double x2 = __shfl_sync(0xffffffffu, mine[2], kLaneOf6[c]);
+      for (int c = 0; c < 4; ++c) {
+        const double x0 = __shfl_sync(0xffffffffu, mine[0], kLaneOf4[c]);
+        const double x1 = __shfl_sync(0xffffffffu, mine[1], kLaneOf4[c]);
+        const double x2 = __shfl_sync(0xffffffffu, mine[2], kLaneOf4[c]);
         part[c] = lane == 0 ? x0 : (lane == 1 ? x1 : x2);
       }
       if (lane < 3 && P.agg) {
-        dd tsum{part[0], 0.0}, esum{part[3], 0.0};
+        dd tsum{part[0], 0.0}, esum{part[2], 0.0};
         dd_add2(tsum, part[1], 0.0);
-        dd_add2(tsum, part[2], 0.0);
-        dd_add2(esum, part[4], 0.0);
-        dd_add2(esum, part[5], 0.0);
+        dd_add2(esum, part[3], 0.0);
         const uint32_t id = lane == 0 ? ired[0] : (lane == 1 ? ired[1] : ired[2]);
         const uint32_t sc = lane == 0 ? ired[3] : (lane == 1 ? ired[4] : ired[5]);
         cs_agg a;
@@ -456,18 +437,31 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t e[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) e[k] = L.entry(u[k]);
+    for (int k = 0; k < 4; ++k) {
+#ifdef CS_DIAG_NO_LUT  // diagnostic build only: replaces the LUT load by arithmetic (wrong bins)
+      e[k] = (((u[k] >> L.s1) & 511u) << 16);
+#else
+      e[k] = L.entry(u[k]);
+#endif
+    }
     uint32_t b[4];
-    if (max(max(e[0], e[1]), max(e[2], e[3])) < kRedirect32) {
-      if (VIO) flags |= e[0] | e[1] | e[2] | e[3];
+    const uint32_t any = e[0] | e[1] | e[2] | e[3];
+    if ((int32_t)any >= 0) {  // no redirect (marker 0xFFFF....; leaves have bit 31 clear while U < 2^15)
+      if (VIO) flags |= any;
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
-    } else {
+    } else {  // redirects (or, for >= 2^15 bins, high bases): deep() re-checks every entry
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = L.deep(e[k], u[k], flags);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) atomicAdd(&h[b[k]], 1u);
+    for (int k = 0; k < 4; ++k) {
+#ifdef CS_DIAG_NO_ATOMS  // diagnostic build only: no histogram update (wrong aggregates)
+      flags ^= b[k] << 1;
+#else
+      atomicAdd(&h[b[k]], 1u);
+#endif
+    }
     const int64_t i0 = s0 + 4 * (int64_t)v;
     if (PEN) {
       uint32_t pb = b[0];  // step 0 is never penalised (sim.py:119)
@@ -559,7 +553,10 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint3
 }
 
 template <typename CapT, bool PEN, bool STEP, bool VIO>
-__global__ void __launch_bounds__(512, 2) eval_kernel(const __grid_constant__ EvalParams P) {
+#ifndef CS_MIN_BLOCKS
+#define CS_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_constant__ EvalParams P) {
   constexpr bool F32 = sizeof(CapT) == 4;
   extern __shared__ __align__(16) unsigned char smem[];
   const DevTables& tb = P.tb;
@@ -805,7 +802,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   pl.seg_len = seg_len;
   pl.ctas = (int)std::max<int64_t>(
       1, std::min<int64_t>((int64_t)nsm * b_per_sm, (a->n_traces * nseg + pl.gpc - 1) / pl.gpc));
-  pl.ws_prep = a16((size_t)(t.seg.size() / 4) * 96);
+  pl.ws_prep = a16((size_t)(t.seg.size() / 4) * 64);
   pl.ws_split = nseg > 1 ? (size_t)a->n_traces *
                                ((size_t)U4 + (pen ? (size_t)M * 3 * U4 : 0) + (size_t)M * 3) * sizeof(uint32_t)
                          : 0;
@@ -871,8 +868,8 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace);
   double2* segrec = reinterpret_cast<double2*>(ws);
   P.segrec = segrec;
-  // bits per exact level: counts up to S must keep count x hi below 2^53 quanta
-  int L = 26;
+  // bits of the exact hi part: counts up to S must keep sum(count x hi) below 2^53 quanta
+  int L = 52;
   while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
   int launches = 0;
   prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, segrec);
