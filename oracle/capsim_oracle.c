@@ -300,3 +300,142 @@ int ora_simulate_batch(const int32_t* mtl, const int32_t* bs, const double* thr,
   free(grids);
   return n_threads;
 }
+
+/* ---- online controller replay (controller.py:96-231), the §8(f) extension ----------------- */
+
+/* CPython's MT19937 (Modules/_randommodule.c): init_by_array seeding, genrand_uint32 and
+ * random() = (a*2^26 + b) / 2^53 from two draws; uniform(a, b) = a + (b - a) * random()
+ * (Lib/random.py). random.Random(seed) for an int seed keys init_by_array with the 32-bit
+ * little-endian words of abs(seed) (at least one word). */
+typedef struct { uint32_t mt[624]; int mti; } ora_mt;
+
+static void ora_mt_init_genrand(ora_mt* s, uint32_t seed) {
+  s->mt[0] = seed;
+  for (int i = 1; i < 624; ++i) s->mt[i] = 1812433253u * (s->mt[i - 1] ^ (s->mt[i - 1] >> 30)) + (uint32_t)i;
+  s->mti = 624;
+}
+
+void ora_mt_seed(ora_mt* s, const uint32_t* key, int key_len) {
+  ora_mt_init_genrand(s, 19650218u);
+  int i = 1, j = 0;
+  for (int k = (624 > key_len ? 624 : key_len); k; --k) {
+    s->mt[i] = (s->mt[i] ^ ((s->mt[i - 1] ^ (s->mt[i - 1] >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
+    ++i, ++j;
+    if (i >= 624) { s->mt[0] = s->mt[623]; i = 1; }
+    if (j >= key_len) j = 0;
+  }
+  for (int k = 623; k; --k) {
+    s->mt[i] = (s->mt[i] ^ ((s->mt[i - 1] ^ (s->mt[i - 1] >> 30)) * 1566083941u)) - (uint32_t)i;
+    ++i;
+    if (i >= 624) { s->mt[0] = s->mt[623]; i = 1; }
+  }
+  s->mt[0] = 0x80000000u;
+  s->mti = 624;
+}
+
+static uint32_t ora_mt_next(ora_mt* s) {
+  static const uint32_t mag01[2] = {0u, 0x9908b0dfu};
+  if (s->mti >= 624) {
+    int kk;
+    uint32_t y;
+    for (kk = 0; kk < 624 - 397; ++kk) {
+      y = (s->mt[kk] & 0x80000000u) | (s->mt[kk + 1] & 0x7fffffffu);
+      s->mt[kk] = s->mt[kk + 397] ^ (y >> 1) ^ mag01[y & 1u];
+    }
+    for (; kk < 623; ++kk) {
+      y = (s->mt[kk] & 0x80000000u) | (s->mt[kk + 1] & 0x7fffffffu);
+      s->mt[kk] = s->mt[kk + (397 - 624)] ^ (y >> 1) ^ mag01[y & 1u];
+    }
+    y = (s->mt[623] & 0x80000000u) | (s->mt[0] & 0x7fffffffu);
+    s->mt[623] = s->mt[396] ^ (y >> 1) ^ mag01[y & 1u];
+    s->mti = 0;
+  }
+  uint32_t y = s->mt[s->mti++];
+  y ^= (y >> 11);
+  y ^= (y << 7) & 0x9d2c5680u;
+  y ^= (y << 15) & 0xefc60000u;
+  y ^= (y >> 18);
+  return y;
+}
+
+double ora_mt_random(ora_mt* s) {
+  uint32_t a = ora_mt_next(s) >> 5, b = ora_mt_next(s) >> 6;
+  return ((double)a * 67108864.0 + (double)b) * (1.0 / 9007199254740992.0);
+}
+
+/* One replay (controller.py:161-231). mode: 0 reactive, 1 proactive(window_k).
+ * initial: caller entry index, or -1 for select_config(first cap).
+ * Per-step outputs (nullable, [n_steps]):
+ *   kind_bits: bit0 violation (VIOLATION_DETECTED + RECONFIGURED), bit1 preemptive reselection
+ *   measured:  measured power fed to the step
+ *   sel_r / cnt_r: selection (+ feasible_count) after the reactive part (current before the
+ *                  step when nothing happened)
+ *   sel_f / cnt_f: selection after the step
+ * Aggregates: violations, reconfigs, avg throughput (fsum/n). Returns 0, or -1 on bad args. */
+int ora_replay(const int32_t* mtl, const int32_t* bs, const double* thr, const double* pw, int n, const double* caps,
+               int64_t n_steps, int mode, int window_k, int32_t initial, double noise_pct, const uint32_t* key,
+               int key_len, uint8_t* kind_bits, double* measured_out, int32_t* sel_r, int64_t* cnt_r,
+               int32_t* sel_f, int64_t* cnt_f, int64_t* violations, int64_t* reconfigs, double* avg) {
+  if (n_steps < 1 || window_k < 1) return -1;
+  double* powers = (double*)malloc(sizeof(double) * (size_t)n);
+  int32_t* best = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  int m = ora_index_build(mtl, bs, thr, pw, n, ORA_COMBINATION, 1, 1, powers, best);
+  ora_mt rng;
+  ora_mt_seed(&rng, key, key_len);
+  double* hist = (double*)malloc(sizeof(double) * (size_t)window_k);
+  int hlen = 0, hpos = 0;
+  int32_t cur;
+  int64_t cur_cnt;
+  if (initial >= 0) {
+    cur = initial;
+    cur_cnt = 0; /* Selection(config, thr, pw): feasible_count defaults to 0 (controller.py:187-189) */
+  } else {
+    cur_cnt = ora_index_select(powers, best, m, caps[0], &cur);
+  }
+  ora_partials tp = {0, 0, 0};
+  int64_t viol = 0, rec = 0;
+  for (int64_t i = 0; i < n_steps; ++i) {
+    const double cap = caps[i];
+    double meas = cur < 0 ? 0.0 : pw[cur];
+    if (noise_pct > 0 && cur >= 0) meas *= 1.0 + ((-noise_pct) + (noise_pct - (-noise_pct)) * ora_mt_random(&rng)) / 100.0;
+    uint8_t kb = 0;
+    if (meas > cap) { /* _reactive_core */
+      kb |= 1;
+      ++viol;
+      cur_cnt = ora_index_select(powers, best, m, cap, &cur);
+      ++rec;
+    }
+    if (sel_r) sel_r[i] = cur;
+    if (cnt_r) cnt_r[i] = cur_cnt;
+    /* cap history (deque maxlen k), appended in both modes */
+    hist[hpos] = cap;
+    hpos = (hpos + 1) % window_k;
+    if (hlen < window_k) ++hlen;
+    if (mode == 1) {
+      /* fmean(history) = fsum(history) / len, oldest first (deque order) */
+      ora_partials ps = {0, 0, 0};
+      int start = hlen < window_k ? 0 : hpos;
+      for (int q = 0; q < hlen; ++q) ora_partials_add(&ps, hist[(start + q) % window_k]);
+      const double predicted = ora_partials_result(&ps) / (double)hlen;
+      free(ps.p);
+      if (cur >= 0 && predicted < pw[cur]) {
+        kb |= 2;
+        cur_cnt = ora_index_select(powers, best, m, predicted, &cur);
+        ++rec;
+      }
+    }
+    if (kind_bits) kind_bits[i] = kb;
+    if (measured_out) measured_out[i] = meas;
+    if (sel_f) sel_f[i] = cur;
+    if (cnt_f) cnt_f[i] = cur_cnt;
+    ora_partials_add(&tp, cur < 0 ? 0.0 : thr[cur]);
+  }
+  *violations = viol;
+  *reconfigs = rec;
+  *avg = ora_partials_result(&tp) / (double)n_steps;
+  free(tp.p);
+  free(hist);
+  free(powers);
+  free(best);
+  return 0;
+}

@@ -83,6 +83,12 @@ def lib():
         L.ora_simulate_batch.argtypes = [i32p, i32p, f64p, f64p, i64p, f64p, C.c_int, f32p, C.c_int64, C.c_int64,
                                          C.c_int32, C.c_double, C.c_int, f64p, i64p, f64p]
         L.ora_simulate_batch.restype = C.c_int
+        u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+        u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+        L.ora_replay.argtypes = [i32p, i32p, f64p, f64p, C.c_int, f64p, C.c_int64, C.c_int, C.c_int, C.c_int32,
+                                 C.c_double, u32p, C.c_int, u8p, f64p, i32p, i64p, i32p, i64p,
+                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        L.ora_replay.restype = C.c_int
         _lib = L
     return _lib
 
@@ -165,3 +171,80 @@ def simulate_batch(grids: list[GridArrays], caps2d: np.ndarray, step_seconds: in
                                     float(switch_penalty_s), int(n_threads), out_avg, out_idle, out_en)
     shp = (t, m, 3)
     return out_avg.reshape(shp), out_idle.reshape(shp), out_en.reshape(shp), used
+
+
+def seed_key(seed: int) -> np.ndarray:
+    """random.Random(seed) key for init_by_array: 32-bit words of abs(seed), >= 1 word."""
+    n = abs(int(seed))
+    words = []
+    while True:
+        words.append(n & 0xFFFFFFFF)
+        n >>= 32
+        if not n:
+            break
+    return np.ascontiguousarray(words, dtype=np.uint32)
+
+
+@dataclass
+class ReplayResult:
+    kind_bits: np.ndarray
+    measured: np.ndarray
+    sel_r: np.ndarray
+    cnt_r: np.ndarray
+    sel_f: np.ndarray
+    cnt_f: np.ndarray
+    violations: int
+    reconfigs: int
+    avg_throughput_ips: float
+    start_sel: int
+    start_cnt: int
+
+
+def replay(g: GridArrays, caps, mode: str, window_k: int = 1, initial: int = -1, noise_pct: float = 0.0,
+           seed: int = 0) -> ReplayResult:
+    """controller.py:161-231 restated (ora_replay). initial: entry index or -1 (auto)."""
+    caps = np.ascontiguousarray(caps, dtype=np.float64)
+    n = caps.shape[0]
+    key = seed_key(seed)
+    kb = np.zeros(n, np.uint8)
+    meas = np.zeros(n, np.float64)
+    sr = np.zeros(n, np.int32)
+    cr = np.zeros(n, np.int64)
+    sf = np.zeros(n, np.int32)
+    cf = np.zeros(n, np.int64)
+    v, r, a = C.c_int64(), C.c_int64(), C.c_double()
+    rc = lib().ora_replay(g.mtl, g.bs, g.thr, g.pw, len(g), caps, n, 1 if mode == "proactive" else 0,
+                          int(window_k), int(initial), float(noise_pct), key, key.shape[0], kb, meas, sr, cr, sf, cf,
+                          C.byref(v), C.byref(r), C.byref(a))
+    if rc != 0:
+        raise ValueError("bad replay arguments")
+    if initial >= 0:
+        s0, c0 = initial, 0
+    else:
+        s0, c0 = Index(g, "combination").select(float(caps[0]))
+    return ReplayResult(kb, meas, sr, cr, sf, cf, int(v.value), int(r.value), a.value, s0, c0)
+
+
+def replay_events(res: ReplayResult, caps, pw) -> tuple[list, list]:
+    """Rebuild the reference's event log and parallel selection list (controller.py:200-218)
+    as ([step, kind, cap, power], [(entry, count) | (-1, 0)])."""
+    events, sels = [], []
+    prior = (res.start_sel, res.start_cnt)
+    for i in range(len(caps)):
+        kb = int(res.kind_bits[i])
+        cap = float(caps[i])
+        rsel = (int(res.sel_r[i]), int(res.cnt_r[i]))
+        fsel = (int(res.sel_f[i]), int(res.cnt_f[i]))
+        if kb & 1:
+            events.append([i, "violation_detected", cap, float(res.measured[i])])
+            sels.append(prior)
+            events.append([i, "reconfigured", cap, 0.0 if rsel[0] < 0 else float(pw[rsel[0]])])
+            sels.append(rsel)
+        else:
+            events.append([i, "no_action", cap, float(res.measured[i])])
+            sels.append(prior)
+        if kb & 2:
+            events.append([i, "preemptive_reconfigured", cap, 0.0 if fsel[0] < 0 else float(pw[fsel[0]])])
+            sels.append(fsel)
+        prior = fsel
+    return events, sels

@@ -110,14 +110,20 @@ __device__ __forceinline__ float gauss(uint64_t h) {
   return (s - 2.0f) * 1.7320508f;
 }
 
-// One warp generates 32 traces (a lane each, sequential in time) and writes 32x32 tiles
-// transposed through shared memory so every store is a coalesced 128-byte row segment.
+// One warp generates 32 traces (a lane each, sequential in time) over one chunk of
+// kGenChunk steps and writes 32x32 tiles transposed through shared memory so every store is a
+// coalesced 128-byte row segment. Chunks run in parallel (blockIdx.y); each starts its AR(1) /
+// OU state from a draw keyed by (seed, trace id, chunk), so the traces stay a pure function of
+// the global trace id.
+constexpr int64_t kGenChunk = 4096;
+
 __global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
                            int32_t kind, float peak, uint64_t seed) {
   __shared__ float tile[8][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32;
   if (t0 >= T) return;
+  const int64_t c0 = (int64_t)blockIdx.y * kGenChunk, c1 = min(S, c0 + kGenChunk);
   const int64_t tid = first_id + t0 + lane;
   const uint64_t hk = splitmix(seed ^ splitmix((uint64_t)tid));
   int k = kind;
@@ -129,8 +135,10 @@ __global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_
   const float a_cloud = __expf(-dt / 3600.0f);                      // 1 h cloud correlation time
   const float wind_mu = 5.0f + 5.0f * u01(splitmix(hk ^ 3));       // mean wind speed (m/s)
   const float theta = 1.0f / 7200.0f;                               // OU mean reversion (1/s)
-  float cloud = 0.6f, wind = wind_mu;
-  for (int64_t s0 = 0; s0 < S; s0 += 32) {
+  const uint64_t hc = splitmix(hk ^ (0xC0FFEEull + (uint64_t)blockIdx.y));
+  float cloud = fminf(fmaxf(0.7f + var * 0.5f * gauss(hc), 0.2f), 1.0f);
+  float wind = fmaxf(wind_mu + var * 4.0f * 0.7f * gauss(splitmix(hc)), 0.0f);
+  for (int64_t s0 = c0; s0 < c1; s0 += 32) {
     for (int j = 0; j < 32; ++j) {
       const int64_t s = s0 + j;
       const uint64_t hs = splitmix(hk ^ (uint64_t)(s * 0x632BE59BD9B4E019ull));
@@ -196,7 +204,10 @@ std::string launch_generate(float* caps, int64_t T, int64_t S, int64_t ld, int64
   if (T <= 0 || S <= 0) return std::string();
   const int64_t warps = (T + 31) / 32;
   const int64_t blocks = (warps + 7) / 8;
-  gen_kernel<<<(unsigned)blocks, 256, 0, st>>>(caps, T, S, ld, first_id, step_seconds, kind, peak, seed);
+  const int64_t chunks = (S + kGenChunk - 1) / kGenChunk;
+  if (chunks > 65535) return "trace too long for the generator (> 65535 chunks)";
+  gen_kernel<<<dim3((unsigned)blocks, (unsigned)chunks), 256, 0, st>>>(caps, T, S, ld, first_id, step_seconds, kind,
+                                                                       peak, seed);
   CS_CUDA_TRY(cudaGetLastError());
   return std::string();
 }

@@ -287,10 +287,56 @@ def synth_golden() -> dict:
     return {"source": "capsim 0.1.0 reference, profile.py:169-215", "grids": out}
 
 
+def controller_golden() -> dict:
+    """controller.replay (controller.py:161-231): events, selections and aggregates."""
+    from capsim.controller import REACTIVE, proactive, replay
+
+    rng = random.Random(9)
+    g1 = build(G1_POINTS)
+    g2 = build({(1, 1): (100.0, 100.0), (1, 2): (180.0, 150.0), (2, 1): (200.0, 240.0), (2, 2): (320.0, 260.0)})
+    cases = [
+        ("g1_rising", g1, [100.0, 150.0, 200.0, 250.0, 300.0], None, "reactive", 1, 0.0, 0),
+        ("g1_fixture_r", g1, [250.0, 250.0, 150.0], (2, 2), "reactive", 1, 0.0, 0),
+        ("g1_fixture_p", g1, [250.0, 250.0, 150.0], (2, 2), "proactive", 2, 0.0, 0),
+        ("g1_flat", g1, [200.0] * 20, None, "proactive", 3, 0.0, 0),
+        ("g1_noise", g1, [200.0, 180.0, 160.0, 220.0, 140.0], None, "reactive", 1, 2.0, 13),
+        ("g1_idle", g1, [250.0, 10.0], (2, 2), "reactive", 1, 0.0, 0),
+        ("g2_pre", g2, [230.0, 250.0, 270.0, 200.0, 150.0, 300.0], (2, 2), "proactive", 3, 0.0, 0),
+    ]
+    for i in range(30):
+        grid = random_grid(rng, tie_heavy=(i % 3 == 0))
+        n = rng.choice([1, 5, 40, 200])
+        caps = [rng.uniform(0.0, 350.0) for _ in range(n)]
+        mode = rng.choice(["reactive", "proactive"])
+        k = rng.randint(1, 6)
+        noise = rng.choice([0.0, 0.5, 2.0, 10.0])
+        seed = rng.choice([0, 1, 5, 123456789, 2**40 + 7, -77, 2**70 + 3])
+        init = None
+        if i % 2 == 0:
+            c = rng.choice(sorted(grid.entries))
+            init = (c.mtl, c.bs)
+        cases.append((f"rand{i}", grid, caps, init, mode, k, noise, seed))
+    docs = []
+    for name, grid, caps, init, mode, k, noise, seed in cases:
+        m = REACTIVE if mode == "reactive" else proactive(k)
+        rep = replay(grid, PowerTrace(name, 60, T0, tuple(caps)), m,
+                     initial_config=None if init is None else Config(*init), noise_pct=noise, seed=seed)
+        docs.append({
+            "name": name, "grid": grid_doc(grid), "caps": caps, "initial": init, "mode": mode, "window_k": k,
+            "noise_pct": noise, "seed": seed,
+            "events": [[e.step_index, e.kind.value, e.cap_w, e.power_w] for e in rep.events],
+            "selections": [sel_doc(s) if s.config is not None else None for s in rep.selections],
+            "violations": rep.violations, "reconfigs": rep.reconfigs,
+            "violation_fraction": rep.violation_fraction, "avg_throughput_ips": rep.avg_throughput_ips,
+            "num_steps": rep.num_steps,
+        })
+    return {"source": "capsim 0.1.0 reference, controller.py:96-231", "cases": docs}
+
+
 def main() -> None:
     print("reference capsim from", capsim.__file__)
     for name, fn in (("policy_golden.json", policy_golden), ("sim_golden.json", sim_golden),
-                     ("synth_golden.json", synth_golden)):
+                     ("synth_golden.json", synth_golden), ("controller_golden.json", controller_golden)):
         doc = fn()
         (OUT / name).write_text(json.dumps(doc, separators=(",", ":")) + "\n")
         print("wrote", name, (OUT / name).stat().st_size, "bytes")
