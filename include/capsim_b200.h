@@ -154,6 +154,32 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* t, const void* caps_host,
                         int64_t ld, int32_t step_seconds, double switch_penalty_s, uint32_t flags, cs_agg* agg_host,
                         uint64_t* hist_host, int64_t* h2d_bytes, int64_t* d2h_bytes);
 
+/* ---- online controller replay: controller.replay (controller.py:161-231), one thread per trace ---- */
+#define CS_CTRL_REACTIVE 0
+#define CS_CTRL_PROACTIVE 1
+typedef struct {
+  double measured_power_w; /* power fed to the step (selection's power x seeded noise) */
+  uint16_t bin_reactive;   /* grid bin of the selection after the reactive part (0xFFFF: initial config) */
+  uint16_t bin_final;      /* grid bin of the selection after the step */
+  uint8_t kind_bits;       /* bit0: VIOLATION_DETECTED + RECONFIGURED; bit1: PREEMPTIVE_RECONFIGURED */
+  uint8_t pad[3];
+} cs_replay_step;
+typedef struct {
+  int64_t violations;        /* ControllerReport.violations */
+  int64_t reconfigs;         /* ControllerReport.reconfigs */
+  double violation_fraction; /* violations / num_steps */
+  double avg_throughput_ips; /* fsum(post-step throughput) / num_steps */
+  int64_t num_steps;
+} cs_replay_agg;
+/* caps_dev: fp64 [n_traces][ld] (tables staged with CS_CAP_F64); initial_dev: nullable int32
+ * [n_traces] entry index per trace (-1: select_config(first cap)); noise: random.Random(seed)
+ * with seed = keys (abs(seed) 32-bit words, key_len words per trace) or, when keys is NULL,
+ * seed_base + trace index. steps_dev nullable [n_traces][n_steps]. */
+int cs_replay(const cs_tables* t, int32_t grid, const double* caps_dev, int64_t n_traces, int64_t n_steps, int64_t ld,
+              int32_t mode, int32_t window_k, const int32_t* initial_dev, double noise_pct, const uint32_t* keys_dev,
+              const int32_t* key_len_dev, int32_t key_stride, uint64_t seed_base, cs_replay_step* steps_dev,
+              cs_replay_agg* agg_dev, void* stream);
+
 /* ---- synthetic traces for benchmarks (counter-based, keyed by (seed, global trace id)) ---- */
 #define CS_TRACE_SOLAR 0
 #define CS_TRACE_WIND 1

@@ -6,10 +6,25 @@ capsim/__init__.py:8-116 for profile tables, power traces, the batching / multi-
 combination policies and simulate(); every decision runs in hand-written sm_100a kernels
 (libcapsim_b200.so via ctypes). Use it as ``import paper_2306_12247_b200 as capsim``.
 
-Out of scope (not accelerated): the online controller, the sampling selector
-and the CLI.
+Also on the GPU: the online controller replay (controller.py).
+Out of scope: the sampling selector and the CLI.
 """
 
+from .controller import (
+    REACTIVE,
+    ControlEvent,
+    ControllerReport,
+    ControllerState,
+    ControlMode,
+    EventKind,
+    event_log_csv_text,
+    moving_average_prediction,
+    proactive,
+    replay,
+    replay_many,
+    step_proactive,
+    step_reactive,
+)
 from .engine import EvalResult, HostEngine, Tables, generate_traces
 from .errors import CapsimError, ParseError, ValidationError
 from .policy import (
@@ -82,4 +97,7 @@ __all__ = [
     "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
     "slice_report", "synthesize_grid", "trace_csv_text", "trace_stats",
     "Tables", "EvalResult", "HostEngine", "generate_traces",
+    "REACTIVE", "ControlEvent", "ControllerReport", "ControllerState", "ControlMode", "EventKind",
+    "event_log_csv_text", "moving_average_prediction", "proactive", "replay", "replay_many", "step_proactive",
+    "step_reactive",
 ]

@@ -36,7 +36,7 @@ EXPORTS = (
     "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches",
     "cs_select_caps", "cs_feasible_caps",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
-    "cs_generate_traces",
+    "cs_replay", "cs_generate_traces",
 )
 
 
@@ -107,6 +107,16 @@ class EvalArgs(C.Structure):
     ]
 
 
+class ReplayStep(C.Structure):
+    _fields_ = [("measured_power_w", C.c_double), ("bin_reactive", C.c_uint16), ("bin_final", C.c_uint16),
+                ("kind_bits", C.c_uint8), ("pad", C.c_uint8 * 3)]
+
+
+class ReplayAgg(C.Structure):
+    _fields_ = [("violations", C.c_int64), ("reconfigs", C.c_int64), ("violation_fraction", C.c_double),
+                ("avg_throughput_ips", C.c_double), ("num_steps", C.c_int64)]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -135,6 +145,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_engine_destroy": ([vp], C.c_int),
         "cs_engine_eval_host": ([vp, vp, vp, i64, i64, i64, i32, dbl, u32, vp, vp, P(i64), P(i64)], C.c_int),
         "cs_generate_traces": ([vp, i64, i64, i64, i64, i32, i32, C.c_float, C.c_uint64, vp], C.c_int),
+        "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

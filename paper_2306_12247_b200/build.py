@@ -20,7 +20,7 @@ LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libcapsim_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["staging.cpp", "capi.cpp", "eval.cu", "aux_kernels.cu"]
+SOURCES = ["staging.cpp", "capi.cpp", "eval.cu", "aux_kernels.cu", "replay.cu"]
 HEADERS = ["cs_internal.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

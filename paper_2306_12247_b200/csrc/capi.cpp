@@ -20,6 +20,10 @@ std::string launch_select(const DevTables& v, int g, int p, const double* caps, 
                           cudaStream_t st);
 std::string launch_feasible(const DevTables& v, int g, int p, const double* caps, int64_t n, uint32_t* mask,
                             cudaStream_t st);
+std::string launch_replay(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld, int mode,
+                          int window_k, const int32_t* initial, double noise_pct, const uint32_t* keys,
+                          const int32_t* key_len, int key_stride, unsigned long long seed_base, cs_replay_step* steps,
+                          cs_replay_agg* agg, cudaStream_t st);
 std::string launch_generate(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
                             int32_t kind, float peak, uint64_t seed, cudaStream_t st);
 
@@ -335,6 +339,27 @@ int cs_feasible_caps(const cs_tables* tp, int32_t grid, int32_t policy, const do
   std::string err = cs::launch_feasible(d->view, grid, policy, caps_dev, n, mask_dev,
                                         reinterpret_cast<cudaStream_t>(stream));
   if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+int cs_replay(const cs_tables* tp, int32_t grid, const double* caps_dev, int64_t n_traces, int64_t n_steps, int64_t ld,
+              int32_t mode, int32_t window_k, const int32_t* initial_dev, double noise_pct, const uint32_t* keys_dev,
+              const int32_t* key_len_dev, int32_t key_stride, uint64_t seed_base, cs_replay_step* steps_dev,
+              cs_replay_agg* agg_dev, void* stream) {
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  if (d->view.cap_dtype != CS_CAP_F64) return fail(CS_E_INVALID, "cs_replay needs tables staged for fp64 caps");
+  if (grid < 0 || grid >= d->view.M) return fail(CS_E_INVALID, "grid out of range");
+  if (n_steps < 1 && n_traces > 0) return fail(CS_E_INVALID, "cannot replay an empty trace");
+  if (ld < n_steps || (mode != CS_CTRL_REACTIVE && mode != CS_CTRL_PROACTIVE) || !(noise_pct >= 0.0) || !agg_dev)
+    return fail(CS_E_INVALID, "bad replay arguments");
+  if (keys_dev && !key_len_dev) return fail(CS_E_INVALID, "keys need key lengths");
+  std::string err = cs::launch_replay(d->view, grid, caps_dev, n_traces, n_steps, ld, mode, window_k, initial_dev,
+                                      noise_pct, keys_dev, key_len_dev, key_stride, seed_base, steps_dev, agg_dev,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(err.rfind("CUDA", 0) == 0 ? CS_E_CUDA : CS_E_INVALID, err);
   return CS_OK;
 }
 

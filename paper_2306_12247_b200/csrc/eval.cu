@@ -80,13 +80,14 @@ struct EvalParams {
   cs_agg* agg;
   unsigned long long* hist;
   uint32_t* part_hist;  // split mode: [T][U]
-  uint32_t* part_sw;    // [T][M*3][U]
+  uint32_t* part_sw;    // [T][NSEG] switched steps per selection segment (PEN)
   uint32_t* part_vio;   // [T][M*3]
   // per selection segment of this launch: {u_lo, u_hi, idle, -} then thr / energy / penalised thr,
   // each split into {hi, mid, lo} with hi and mid on fixed quantum grids so that count x hi and
   // count x mid accumulate EXACTLY (6 x 16 B per segment, see prep_kernel)
   const double2* segrec;
-  int32_t U4;  // histogram row stride (U rounded up to a multiple of 4)
+  int32_t U4;    // histogram row stride (U rounded up to a multiple of 4)
+  int32_t NSEG;  // selection segments over all grids x policies
   double omp;
   int32_t wpg, gpc;
   // shared-memory layout (bytes)
@@ -243,7 +244,7 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
     for (int p = 0; p < 3; ++p) {
       const int mp = 3 * m + p;
       const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
-      const uint32_t* sw = PEN ? SW + (size_t)mp * P.U4 : nullptr;
+      const uint32_t* sw = PEN ? SW + k0 : nullptr;  // switched steps per segment of (m, p)
       double a[4] = {0.0, 0.0, 0.0, 0.0};  // thr hi, lo, energy hi, lo
       uint32_t idle = 0, swc = 0;
       for (int k = k0 + gtid; k < k1; k += gsize) {
@@ -257,7 +258,7 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
         a[3] = __fma_rn(dc, ve.y, a[3]);
         uint32_t scnt = 0;
         if (PEN) {
-          scnt = sw[sg.y] - (sg.x ? sw[sg.x - 1] : 0u);
+          scnt = sw[k - k0];
           swc += scnt;
         }
         if (sg.z) {
@@ -339,16 +340,12 @@ __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uin
   const int U4 = P.U4, M = P.tb.M;
   uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then partial sums
   group_scan(h, U4, ghist, wtot, gtid, gsize, gid_local);
-  if (PEN)
-    for (int mp = 0; mp < M * 3; ++mp)
-      group_scan(sw + (size_t)mp * U4, U4, (uint32_t*)nullptr, wtot, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
   epilogue<PEN>(P, t, h, sw, vcnt, scratch, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
   for (int u = 4 * gtid; u < U4; u += 4 * gsize) *reinterpret_cast<uint4*>(h + u) = make_uint4(0u, 0u, 0u, 0u);
   if (PEN)
-    for (int i = 4 * gtid; i < M * 3 * U4; i += 4 * gsize)
-      *reinterpret_cast<uint4*>(sw + i) = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
 }
 
 // Exact violation recount of a segment (slow path; only runs if the fast check fired).
@@ -418,7 +415,8 @@ template <bool PEN, bool STEP, bool VIO>
 __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* sw,
                                                 const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
                                                 int gsize) {
-  const int U = P.tb.U, U4 = P.U4, M = P.tb.M;
+  const int U = P.tb.U, M = P.tb.M;
+  const int32_t* s_segoff = reinterpret_cast<const int32_t*>(s_sig + (size_t)M * U);
   const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
@@ -430,7 +428,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
         const uint64_t xo = s_sig[(size_t)m * U + cb] ^ s_sig[(size_t)m * U + pb];
 #pragma unroll
         for (int p = 0; p < 3; ++p)
-          if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * U4 + cb], 1u);
+          if ((xo >> (16 * p)) & 0xFFFFull)
+            atomicAdd(&sw[s_segoff[m * 3 + p] + (int)((s_sig[(size_t)m * U + cb] >> (16 * p)) & 0xFFFFull)], 1u);
       }
   };
   auto vec4 = [&](const uint4 raw, int v) {
@@ -515,6 +514,7 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint3
                                                 int64_t s0, int64_t s1e, int gtid, int gsize) {
   const DevTables& tb = P.tb;
   const int U = tb.U, M = tb.M;
+  const int32_t* s_segoff = reinterpret_cast<const int32_t*>(s_sig + (size_t)M * U);
   const unsigned long long* row = reinterpret_cast<const unsigned long long*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
@@ -531,7 +531,8 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint3
         for (int m = 0; m < M; ++m) {
           const uint64_t xo = s_sig[(size_t)m * U + b] ^ s_sig[(size_t)m * U + pb];
           for (int p = 0; p < 3; ++p)
-            if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[((size_t)m * 3 + p) * P.U4 + b], 1u);
+            if ((xo >> (16 * p)) & 0xFFFFull)
+              atomicAdd(&sw[s_segoff[m * 3 + p] + (int)((s_sig[(size_t)m * U + b] >> (16 * p)) & 0xFFFFull)], 1u);
         }
     }
     if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
@@ -570,8 +571,11 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
   if (!F32 && VIO)
     for (int i = threadIdx.x; i < U; i += blockDim.x) s_vio[i] = __ldg(tb.vio + i);
   uint64_t* s_sig = reinterpret_cast<uint64_t*>(smem + P.off_sig);
-  if (PEN)
+  int32_t* s_segoff = reinterpret_cast<int32_t*>(s_sig + (size_t)M * U);  // [M*3+1] (PEN)
+  if (PEN) {
     for (int i = threadIdx.x; i < M * U; i += blockDim.x) s_sig[i] = __ldg(tb.sig + i);
+    for (int i = threadIdx.x; i <= M * 3; i += blockDim.x) s_segoff[i] = __ldg(tb.seg_off + i);
+  }
   // CTA-level global histogram in 32-bit counters (native shared atomics); a group that would
   // push the CTA's running step count past 2^31 first drains the counters into the global u64
   // histogram (atomicExch, so concurrent groups lose nothing).
@@ -594,7 +598,7 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
   const int U4 = P.U4;
   for (int u = gtid; u < U4; u += gsize) h[u] = 0u;
   if (PEN)
-    for (int i = gtid; i < M * 3 * U4; i += gsize) sw[i] = 0u;
+    for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
   if (gtid < M * 3) vcnt[gtid] = 0u;
   if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag
   __syncthreads();
@@ -649,16 +653,16 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
         if (c) {
           atomicAdd(&P.part_hist[t * U4 + u], c);
           h[u] = 0u;
-          if (PEN)
-            for (int mp = 0; mp < M * 3; ++mp) {
-              const uint32_t s = sw[(size_t)mp * U4 + u];
-              if (s) {
-                atomicAdd(&P.part_sw[(t * M * 3 + mp) * U4 + u], s);
-                sw[(size_t)mp * U4 + u] = 0u;
-              }
-            }
         }
       }
+      if (PEN)
+        for (int i = gtid; i < P.NSEG; i += gsize) {
+          const uint32_t sv = sw[i];
+          if (sv) {
+            atomicAdd(&P.part_sw[t * P.NSEG + i], sv);
+            sw[i] = 0u;
+          }
+        }
       if (gtid < M * 3 && vcnt[gtid]) atomicAdd(&P.part_vio[t * M * 3 + gtid], vcnt[gtid]);
     }
     group_sync(gid_local, gsize);
@@ -681,7 +685,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
   const int64_t t = blockIdx.x;
   const int U4 = P.U4, M = P.tb.M;
   uint32_t* h = P.part_hist + t * U4;
-  uint32_t* sw = PEN ? P.part_sw + t * (int64_t)M * 3 * U4 : nullptr;
+  uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
   const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
   finish_trace<PEN>(P, t, h, sw, vc, P.hist, scratch, threadIdx.x, blockDim.x, 0);
 }
@@ -743,14 +747,15 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   const size_t lut_bytes = a16((size_t)t.lut.size() * 4);
   const size_t vio_bytes = (vio && !f32) ? a16((size_t)U * 8) : 0;
   const int U4 = (U + 3) & ~3;
-  const size_t sig_bytes = pen ? a16((size_t)M * U * 8) : 0;
+  const int nsegs = (int)(t.seg.size() / 4);
+  const size_t sig_bytes = pen ? a16((size_t)M * U * 8 + (size_t)(M * 3 + 1) * 4) : 0;
   const size_t gh_bytes = a->hist ? a16((size_t)U * 4 + 4) : 0;
   const size_t fixed = lut_bytes + vio_bytes + sig_bytes + gh_bytes;
   const int hs = 1;
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
     size_t gb = a16((size_t)U4 * 4 * hs);
     *off_sw = gb;
-    gb += pen ? a16((size_t)M * 3 * U4 * 4) : 0;
+    gb += pen ? a16((size_t)nsegs * 4) : 0;
     *off_v = gb;
     gb += a16((size_t)(M * 3 + 1) * 4);
     *off_scr = gb;
@@ -804,7 +809,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
       1, std::min<int64_t>((int64_t)nsm * b_per_sm, (a->n_traces * nseg + pl.gpc - 1) / pl.gpc));
   pl.ws_prep = a16((size_t)(t.seg.size() / 4) * 64);
   pl.ws_split = nseg > 1 ? (size_t)a->n_traces *
-                               ((size_t)U4 + (pen ? (size_t)M * 3 * U4 : 0) + (size_t)M * 3) * sizeof(uint32_t)
+                               ((size_t)U4 + (pen ? (size_t)nsegs : 0) + (size_t)M * 3) * sizeof(uint32_t)
                          : 0;
 
   EvalParams& P = pl.P;
@@ -830,6 +835,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.gpc = pl.gpc;
   P.hstride = hs;
   P.U4 = U4;
+  P.NSEG = nsegs;
   P.off_vio = (int32_t)lut_bytes;
   P.off_sig = (int32_t)(lut_bytes + vio_bytes);
   P.off_ghist = (int32_t)(lut_bytes + vio_bytes + sig_bytes);
@@ -880,7 +886,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
     uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);
     P.part_hist = w;
     P.part_sw = w + (size_t)a->n_traces * P.U4;
-    P.part_vio = P.part_sw + (pen ? (size_t)a->n_traces * t.M * 3 * P.U4 : 0);
+    P.part_vio = P.part_sw + (pen ? (size_t)a->n_traces * P.NSEG : 0);
     CS_CUDA_TRY(cudaMemsetAsync(w, 0, pl.ws_split, st));
   }
   void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio);
