@@ -180,6 +180,18 @@ int cs_replay(const cs_tables* t, int32_t grid, const double* caps_dev, int64_t 
               const int32_t* key_len_dev, int32_t key_stride, uint64_t seed_base, cs_replay_step* steps_dev,
               cs_replay_agg* agg_dev, void* stream);
 
+/* ---- sampling selector: select_sampling (policy.py:218-273) at every (trace, step) ---- */
+#define CS_SAMPLING_MAX_BUDGET 256
+/* caps_dev: fp64 [n_traces][ld] (tables staged with CS_CAP_F64). Step i of every trace samples
+ * with random.Random(seed_base + i), seed_base the signed 128-bit integer seed_hi:seed_lo;
+ * simulate() passes seed * 1_000_003 (sim.py:159-163), select_sampling(seed) one step with
+ * seed_base = seed. out_entry_dev: int32 [n_traces][n_steps] caller entry index or -1 (idle);
+ * out_count_dev (nullable): int32 feasible_count. budget_m >= 1, rounds_r >= 0; a budget above
+ * CS_SAMPLING_MAX_BUDGET is CS_E_UNSUPPORTED unless it covers every entry of the grid. */
+int cs_select_sampling(const cs_tables* t, int32_t grid, const double* caps_dev, int64_t n_traces, int64_t n_steps,
+                       int64_t ld, int64_t budget_m, int64_t rounds_r, uint64_t seed_lo, int64_t seed_hi,
+                       int32_t* out_entry_dev, int32_t* out_count_dev, void* stream);
+
 /* ---- synthetic traces for benchmarks (counter-based, keyed by (seed, global trace id)) ---- */
 #define CS_TRACE_SOLAR 0
 #define CS_TRACE_WIND 1

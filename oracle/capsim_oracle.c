@@ -439,3 +439,137 @@ int ora_replay(const int32_t* mtl, const int32_t* bs, const double* thr, const d
   free(best);
   return 0;
 }
+
+/* ---- sampling selector (policy.py:191-273), the §8(f) rank-2 extension -------------------- */
+
+/* Random._randbelow_with_getrandbits (Lib/random.py): k = n.bit_length(); r = getrandbits(k)
+ * (= genrand_uint32() >> (32 - k) for k <= 32) until r < n. */
+static uint32_t ora_randbelow(ora_mt* s, uint32_t n) {
+  int k = 0;
+  while (k < 32 && (n >> k)) ++k;
+  uint32_t r = ora_mt_next(s) >> (32 - k);
+  while (r >= n) r = ora_mt_next(s) >> (32 - k);
+  return r;
+}
+
+/* Random.sample's table-size rule: setsize = 21 (+ 4 ** ceil(log(3k, 4)) when k > 5). */
+static int64_t ora_sample_setsize(int64_t k) {
+  int64_t setsize = 21;
+  if (k > 5) {
+    int64_t p = 1;
+    while (p < 3 * k) p *= 4;
+    setsize += p;
+  }
+  return setsize;
+}
+
+/* policy.py:191-197 _nearest_bs: present bs closest to target (excluding `exclude`), ties to
+ * the smaller size; -1 when none. bs values are small integers, so |b - target| is exact. */
+static int32_t ora_nearest_bs(const int32_t* mtl, const int32_t* bs, int n, int32_t at_mtl, double target,
+                              int32_t exclude) {
+  int32_t best = -1;
+  double bd = 0.0;
+  for (int i = 0; i < n; ++i) {
+    if (mtl[i] != at_mtl || bs[i] == exclude) continue;
+    const double d = fabs((double)bs[i] - target);
+    if (best < 0 || d < bd || (d == bd && bs[i] < best)) best = bs[i], bd = d;
+  }
+  return best;
+}
+
+static int ora_find(const int32_t* mtl, const int32_t* bs, int n, int32_t m, int32_t b) {
+  for (int i = 0; i < n; ++i)
+    if (mtl[i] == m && bs[i] == b) return i;
+  return -1;
+}
+
+/* policy.py:200-215 _neighbors: (mtl -/+ 1, same bs) then (same mtl, nearest bs to bs/2, bs*2). */
+static int ora_neighbors(const int32_t* mtl, const int32_t* bs, int n, int c, int out[4]) {
+  int k = 0;
+  for (int d = -1; d <= 1; d += 2) {
+    const int32_t m = mtl[c] + d;
+    if (m < 1) continue;
+    const int e = ora_find(mtl, bs, n, m, bs[c]);
+    if (e >= 0) out[k++] = e;
+  }
+  const double targets[2] = {(double)bs[c] / 2.0, (double)bs[c] * 2.0};
+  for (int q = 0; q < 2; ++q) {
+    const int32_t b = ora_nearest_bs(mtl, bs, n, mtl[c], targets[q], bs[c]);
+    if (b < 0) continue;
+    const int e = ora_find(mtl, bs, n, mtl[c], b);
+    int dup = 0;
+    for (int j = 0; j < k; ++j) dup |= out[j] == e;
+    if (e >= 0 && !dup) out[k++] = e;
+  }
+  return k;
+}
+
+/* policy.py:218-273 select_sampling for one cap (caller validated budget >= 1, rounds >= 0,
+ * cap >= 0). key/key_len: random.Random(seed)'s init_by_array key (seed_key). Returns the
+ * caller index of the selection or -1 (IDLE_SELECTION); *count = len(feasible). */
+int32_t ora_select_sampling(const int32_t* mtl, const int32_t* bs, const double* thr, const double* pw, int n,
+                            int64_t budget_m, int64_t rounds_r, double cap, const uint32_t* key, int key_len,
+                            int64_t* count) {
+  ora_entry* f = (ora_entry*)malloc(sizeof(ora_entry) * (size_t)(n > 0 ? n : 1));
+  int nf = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!(pw[i] <= cap)) continue;
+    f[nf].mtl = mtl[i]; f[nf].bs = bs[i]; f[nf].thr = thr[i]; f[nf].pw = pw[i]; f[nf].idx = i;
+    ++nf;
+  }
+  *count = nf;
+  if (nf == 0) { free(f); return -1; }
+  qsort(f, (size_t)nf, sizeof(ora_entry), ora_qsort_cmp); /* policy.py:246 */
+  int best;
+  if (budget_m >= nf) {
+    best = 0;
+    for (int i = 1; i < nf; ++i) if (!ora_prefer_a(&f[best], &f[i])) best = i;
+  } else {
+    /* rng.sample(feasible, budget_m) (Lib/random.py Random.sample) */
+    ora_mt rng;
+    ora_mt_seed(&rng, key, key_len);
+    const int64_t k = budget_m;
+    int32_t* picked = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);
+    if (nf <= ora_sample_setsize(k)) {
+      int32_t* pool = (int32_t*)malloc(sizeof(int32_t) * (size_t)nf);
+      for (int i = 0; i < nf; ++i) pool[i] = i;
+      for (int64_t i = 0; i < k; ++i) {
+        const uint32_t j = ora_randbelow(&rng, (uint32_t)(nf - i));
+        picked[i] = pool[j];
+        pool[j] = pool[nf - i - 1];
+      }
+      free(pool);
+    } else {
+      uint8_t* sel = (uint8_t*)calloc((size_t)nf, 1);
+      for (int64_t i = 0; i < k; ++i) {
+        uint32_t j = ora_randbelow(&rng, (uint32_t)nf);
+        while (sel[j]) j = ora_randbelow(&rng, (uint32_t)nf);
+        sel[j] = 1;
+        picked[i] = (int32_t)j;
+      }
+      free(sel);
+    }
+    best = picked[0];
+    for (int64_t i = 1; i < k; ++i) if (!ora_prefer_a(&f[best], &f[picked[i]])) best = picked[i];
+    free(picked);
+  }
+  int cur = f[best].idx;
+  free(f);
+  /* hill climb (policy.py:255-266): best feasible strictly-better neighbour, until none */
+  for (int64_t r = 0; r < rounds_r; ++r) {
+    int nb[4];
+    const int k = ora_neighbors(mtl, bs, n, cur, nb);
+    int move = -1;
+    for (int q = 0; q < k; ++q) {
+      const int e = nb[q];
+      if (pw[e] > cap || thr[e] <= thr[cur]) continue;
+      if (move < 0) { move = e; continue; }
+      ora_entry a = {mtl[move], bs[move], thr[move], pw[move], move};
+      ora_entry b = {mtl[e], bs[e], thr[e], pw[e], e};
+      if (!ora_prefer_a(&a, &b)) move = e;
+    }
+    if (move < 0) break;
+    cur = move;
+  }
+  return cur;
+}

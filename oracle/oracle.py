@@ -89,6 +89,9 @@ def lib():
                                  C.c_double, u32p, C.c_int, u8p, f64p, i32p, i64p, i32p, i64p,
                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.ora_replay.restype = C.c_int
+        L.ora_select_sampling.argtypes = [i32p, i32p, f64p, f64p, C.c_int, C.c_int64, C.c_int64, C.c_double, u32p,
+                                          C.c_int, C.POINTER(C.c_int64)]
+        L.ora_select_sampling.restype = C.c_int32
         _lib = L
     return _lib
 
@@ -248,3 +251,32 @@ def replay_events(res: ReplayResult, caps, pw) -> tuple[list, list]:
             sels.append(fsel)
         prior = fsel
     return events, sels
+
+
+def select_sampling(g: GridArrays, budget_m: int, rounds_r: int, cap: float, seed: int) -> tuple[int, int]:
+    """policy.py:218-273 restated (ora_select_sampling) -> (entry index or -1, feasible_count)."""
+    if budget_m < 1 or rounds_r < 0 or cap < 0:
+        raise ValueError("bad sampling arguments")
+    key = seed_key(seed)
+    cnt = C.c_int64()
+    e = lib().ora_select_sampling(g.mtl, g.bs, g.thr, g.pw, len(g), int(budget_m), int(rounds_r), float(cap), key,
+                                  key.shape[0], C.byref(cnt))
+    return int(e), int(cnt.value)
+
+
+SEED_STRIDE = 1_000_003  # sim.py:33-35
+
+
+def simulate_sampling(g: GridArrays, caps, budget_m: int, rounds_r: int, seed: int, step_seconds: int,
+                      switch_penalty_s: float = 0.0) -> SimResult:
+    """sim.py:159-163 + _aggregate: per-step select_sampling with seed*1_000_003 + step."""
+    caps = np.ascontiguousarray(caps, dtype=np.float64)
+    s = caps.shape[0]
+    sel = np.zeros(max(s, 1), dtype=np.int32)
+    cnt = np.zeros(max(s, 1), dtype=np.int64)
+    for i in range(s):
+        sel[i], cnt[i] = select_sampling(g, budget_m, rounds_r, float(caps[i]), seed * SEED_STRIDE + i)
+    avg, idle, en = C.c_double(), C.c_int64(), C.c_double()
+    lib().ora_aggregate(g.thr, g.pw, sel, s, int(step_seconds), float(g.idle_power_w), float(switch_penalty_s),
+                        C.byref(avg), C.byref(idle), C.byref(en))
+    return SimResult(sel[:s], cnt[:s], avg.value, int(idle.value), en.value)

@@ -6,8 +6,9 @@ capsim/__init__.py:8-116 for profile tables, power traces, the batching / multi-
 combination policies and simulate(); every decision runs in hand-written sm_100a kernels
 (libcapsim_b200.so via ctypes). Use it as ``import paper_2306_12247_b200 as capsim``.
 
-Also on the GPU: the online controller replay (controller.py).
-Out of scope: the sampling selector and the CLI.
+Also on the GPU: the online controller replay (controller.py) and the
+sampling selector (select_sampling / simulate with sampling_policy, §8(f) rank 2).
+Out of scope: the CLI.
 """
 
 from .controller import (
@@ -39,6 +40,7 @@ from .policy import (
     feasible_set,
     improvement_pct,
     sampling_policy,
+    sampling_steps,
     select_config,
     select_configs,
     select_sampling,
@@ -93,7 +95,7 @@ __all__ = [
     "REPORT_SCHEMA",
     "compare", "comparison_csv_text", "compute_throughput", "feasible_set", "grid_csv_text", "improvement_pct",
     "load_grid", "load_report", "load_trace", "normalize_display", "normalize_trace", "profiling_cost",
-    "report_from_dict", "report_json_text", "report_to_dict", "sampling_policy", "save_grid", "save_report",
+    "report_from_dict", "report_json_text", "report_to_dict", "sampling_policy", "sampling_steps", "save_grid", "save_report",
     "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
     "slice_report", "synthesize_grid", "trace_csv_text", "trace_stats",
     "Tables", "EvalResult", "HostEngine", "generate_traces",

@@ -19,6 +19,7 @@ CS_OK = 0
 CS_E_INVALID = -1
 CS_E_CUDA = -2
 CS_E_NODEVICE = -3
+CS_E_UNSUPPORTED = -4
 
 CS_CAP_F32 = 0
 CS_CAP_F64 = 1
@@ -36,7 +37,7 @@ EXPORTS = (
     "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches",
     "cs_select_caps", "cs_feasible_caps",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
-    "cs_replay", "cs_generate_traces",
+    "cs_replay", "cs_generate_traces", "cs_select_sampling",
 )
 
 
@@ -146,6 +147,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_engine_eval_host": ([vp, vp, vp, i64, i64, i64, i32, dbl, u32, vp, vp, P(i64), P(i64)], C.c_int),
         "cs_generate_traces": ([vp, i64, i64, i64, i64, i32, i32, C.c_float, C.c_uint64, vp], C.c_int),
         "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),
+        "cs_select_sampling": ([vp, i32, vp, i64, i64, i64, i64, i64, C.c_uint64, i64, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -185,4 +187,6 @@ def check(rc: int, invalid: type[Exception] = ValueError) -> None:
         raise invalid(msg)
     if rc == CS_E_NODEVICE:
         raise NativeLibraryError(msg)
+    if rc == CS_E_UNSUPPORTED:
+        raise NotImplementedError(msg)
     raise CudaError(msg)

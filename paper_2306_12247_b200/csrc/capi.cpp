@@ -20,6 +20,9 @@ std::string launch_select(const DevTables& v, int g, int p, const double* caps, 
                           cudaStream_t st);
 std::string launch_feasible(const DevTables& v, int g, int p, const double* caps, int64_t n, uint32_t* mask,
                             cudaStream_t st);
+std::string launch_sampling(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld,
+                            int64_t budget, int64_t rounds, unsigned long long seed_lo, long long seed_hi,
+                            int32_t* out_entry, int32_t* out_count, int sm_count, cudaStream_t st);
 std::string launch_replay(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld, int mode,
                           int window_k, const int32_t* initial, double noise_pct, const uint32_t* keys,
                           const int32_t* key_len, int key_stride, unsigned long long seed_base, cs_replay_step* steps,
@@ -79,6 +82,9 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
       {t.e_pw.data(), t.e_pw.size() * 8, 0},
       {t.seg_off.data(), t.seg_off.size() * 4, 0},
       {t.seg.data(), t.seg.size() * 4, 0},
+      {t.csort.data(), t.csort.size() * 4, 0},
+      {t.ccnt.data(), t.ccnt.size() * 4, 0},
+      {t.nbr.data(), t.nbr.size() * 4, 0},
   };
   size_t total = 0;
   for (auto& p : parts) {
@@ -133,6 +139,9 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
   v.e_pw = reinterpret_cast<const double*>(b + parts[13].off);
   v.seg_off = reinterpret_cast<const int32_t*>(b + parts[14].off);
   v.seg = reinterpret_cast<const int4*>(b + parts[15].off);
+  v.csort = reinterpret_cast<const int32_t*>(b + parts[16].off);
+  v.ccnt = reinterpret_cast<const int32_t*>(b + parts[17].off);
+  v.nbr = reinterpret_cast<const int32_t*>(b + parts[18].off);
   t.devs.push_back(d);
   *out = &t.devs.back();
   return CS_OK;
@@ -360,6 +369,34 @@ int cs_replay(const cs_tables* tp, int32_t grid, const double* caps_dev, int64_t
                                       noise_pct, keys_dev, key_len_dev, key_stride, seed_base, steps_dev, agg_dev,
                                       reinterpret_cast<cudaStream_t>(stream));
   if (!err.empty()) return fail(err.rfind("CUDA", 0) == 0 ? CS_E_CUDA : CS_E_INVALID, err);
+  return CS_OK;
+}
+
+int cs_select_sampling(const cs_tables* tp, int32_t grid, const double* caps_dev, int64_t n_traces, int64_t n_steps,
+                       int64_t ld, int64_t budget_m, int64_t rounds_r, uint64_t seed_lo, int64_t seed_hi,
+                       int32_t* out_entry_dev, int32_t* out_count_dev, void* stream) {
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (d->view.cap_dtype != CS_CAP_F64) return fail(CS_E_INVALID, "cs_select_sampling needs tables staged for fp64 caps");
+  if (grid < 0 || grid >= d->view.M) return fail(CS_E_INVALID, "grid out of range");
+  if (budget_m < 1) return fail(CS_E_INVALID, "budget_m must be >= 1, got " + std::to_string(budget_m));
+  if (rounds_r < 0) return fail(CS_E_INVALID, "rounds_r must be >= 0, got " + std::to_string(rounds_r));
+  if (n_traces < 0 || n_steps < 0 || ld < n_steps || (!caps_dev && n_traces * n_steps > 0) ||
+      (!out_entry_dev && n_traces * n_steps > 0))
+    return fail(CS_E_INVALID, "bad sampling arguments");
+  const int64_t n_entries = t.e_off[grid + 1] - t.e_off[grid];
+  if (budget_m > CS_SAMPLING_MAX_BUDGET && budget_m < n_entries)
+    return fail(CS_E_UNSUPPORTED, "sampling budgets above " + std::to_string(CS_SAMPLING_MAX_BUDGET) +
+                                      " that do not cover the whole grid are not supported");
+  int sms = 0;
+  CS_CUDA_RET(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::string err = cs::launch_sampling(d->view, grid, caps_dev, n_traces, n_steps, ld, budget_m, rounds_r, seed_lo,
+                                        seed_hi, out_entry_dev, out_count_dev, sms,
+                                        reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(CS_E_CUDA, err);
   return CS_OK;
 }
 

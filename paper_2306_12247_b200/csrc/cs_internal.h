@@ -114,6 +114,10 @@ struct DevTables {
   const int32_t* e_bs;
   const double* e_thr;
   const double* e_pw;
+  // sampling selector (policy.py:191-273)
+  const int32_t* csort;    // [e_off[M]] per grid: caller index of the j-th entry in (power, mtl, bs) order
+  const int32_t* ccnt;     // [M][maxB] combination feasible count per grid bin
+  const int32_t* nbr;      // [e_off[M]][4] present neighbours (caller index, -1 pad)   policy.py:200-215
 };
 
 // Host-side staged tables (cs_tables in the C ABI).
@@ -135,6 +139,7 @@ struct Tables {
   std::vector<uint64_t> vio;          // [U]
   std::vector<int32_t> e_off, e_mtl, e_bs;
   std::vector<double> e_thr, e_pw;
+  std::vector<int32_t> csort, ccnt, nbr;
   // LUT
   int64_t lo = 0, hi = 0;
   uint64_t kbase = 0;

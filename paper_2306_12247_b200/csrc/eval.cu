@@ -417,6 +417,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
                                                 int gsize) {
   const int U = P.tb.U, M = P.tb.M;
   const int32_t* s_segoff = reinterpret_cast<const int32_t*>(s_sig + (size_t)M * U);
+  int so[3] = {0, 0, 0};
+  if (PEN) so[0] = s_segoff[0], so[1] = s_segoff[1], so[2] = s_segoff[2];
   const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
@@ -468,10 +470,29 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
         uint32_t dummy = 0;
         pb = L.bin(__ldg(row + i0 - 1), dummy);
       }
-      switches(b[0], pb);
-      switches(b[1], b[0]);
-      switches(b[2], b[1]);
-      switches(b[3], b[2]);
+      if (M == 1) {  // one signature load per step, chained through the vector
+        uint64_t sg[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sg[k] = s_sig[b[k]];
+        const uint64_t sp = pb == b[0] ? sg[0] : s_sig[pb];
+        auto sw1 = [&](uint64_t sc, uint64_t sprev) {
+          const uint64_t xo = sc ^ sprev;
+          if (xo) {
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+              if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[so[p] + (int)((sc >> (16 * p)) & 0xFFFFull)], 1u);
+          }
+        };
+        sw1(sg[0], sp);
+        sw1(sg[1], sg[0]);
+        sw1(sg[2], sg[1]);
+        sw1(sg[3], sg[2]);
+      } else {
+        switches(b[0], pb);
+        switches(b[1], b[0]);
+        switches(b[2], b[1]);
+        switches(b[3], b[2]);
+      }
     }
     if (STEP) {
       uint2 o;

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "cs_internal.h"
+#include "cs_mt.cuh"
 
 namespace cs {
 namespace {
@@ -21,51 +22,6 @@ namespace {
     cudaError_t e_ = (x);                                                                               \
     if (e_ != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #x ")"; \
   } while (0)
-
-struct Mt {
-  uint32_t mt[624];
-  int mti;
-};
-
-__device__ void mt_seed(Mt& s, const uint32_t* key, int key_len) {
-  s.mt[0] = 19650218u;
-  for (int i = 1; i < 624; ++i) s.mt[i] = 1812433253u * (s.mt[i - 1] ^ (s.mt[i - 1] >> 30)) + (uint32_t)i;
-  int i = 1, j = 0;
-  for (int k = 624 > key_len ? 624 : key_len; k; --k) {
-    s.mt[i] = (s.mt[i] ^ ((s.mt[i - 1] ^ (s.mt[i - 1] >> 30)) * 1664525u)) + key[j] + (uint32_t)j;
-    ++i, ++j;
-    if (i >= 624) s.mt[0] = s.mt[623], i = 1;
-    if (j >= key_len) j = 0;
-  }
-  for (int k = 623; k; --k) {
-    s.mt[i] = (s.mt[i] ^ ((s.mt[i - 1] ^ (s.mt[i - 1] >> 30)) * 1566083941u)) - (uint32_t)i;
-    ++i;
-    if (i >= 624) s.mt[0] = s.mt[623], i = 1;
-  }
-  s.mt[0] = 0x80000000u;
-  s.mti = 624;
-}
-
-__device__ uint32_t mt_next(Mt& s) {
-  if (s.mti >= 624) {
-    for (int kk = 0; kk < 624; ++kk) {
-      const uint32_t y = (s.mt[kk] & 0x80000000u) | (s.mt[(kk + 1) % 624] & 0x7fffffffu);
-      s.mt[kk] = s.mt[(kk + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
-    }
-    s.mti = 0;
-  }
-  uint32_t y = s.mt[s.mti++];
-  y ^= (y >> 11);
-  y ^= (y << 7) & 0x9d2c5680u;
-  y ^= (y << 15) & 0xefc60000u;
-  y ^= (y >> 18);
-  return y;
-}
-
-__device__ double mt_random(Mt& s) {
-  const uint32_t a = mt_next(s) >> 5, b = mt_next(s) >> 6;
-  return __dmul_rn(__dadd_rn(__dmul_rn((double)a, 67108864.0), (double)b), 1.0 / 9007199254740992.0);
-}
 
 __device__ __forceinline__ void two_sum_acc(double& hi, double& lo, double v) {
   const double s = __dadd_rn(hi, v);

@@ -1,0 +1,180 @@
+// Sampling selector on the GPU (reference policy.py:191-273, sim.py:159-163).
+//
+// select_sampling(grid, m, r, cap, seed) for every (trace, step) of a cap matrix, one thread per
+// step (steps are independent: each draws from its own random.Random(seed * 1_000_003 + step)).
+// A step is:
+//   1. count = len(feasible) from the staged fp64 rank tables (one LUT search, as PolicyIndex);
+//      the feasible list sorted by (power, mtl, bs) (policy.py:246) is the grid's combination
+//      order csort[0 .. count), so no per-step filter or sort is needed;
+//   2. count == 0 -> idle; m >= count -> every feasible entry is a sample, so the best one is the
+//      combination selection (and no neighbour can improve on a global maximum);
+//   3. otherwise random.sample(range(count), m) replayed bit for bit (Lib/random.py: the pool
+//      branch when count <= setsize, else the rejection-set branch; both hold at most m
+//      positions, so the per-thread state is O(m), not O(count)), best = highest throughput,
+//      ties to the lower sorted position (_prefer, policy.py:88-97);
+//   4. up to r hill-climb rounds over the staged neighbour lists (policy.py:255-266).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "cs_internal.h"
+#include "cs_mt.cuh"
+
+namespace cs {
+namespace {
+
+constexpr int kMaxBudget = CS_SAMPLING_MAX_BUDGET;
+
+struct SampleParams {
+  DevTables tb;
+  int g;
+  const double* caps;
+  int64_t T, S, ld;
+  int64_t budget, rounds, setsize;
+  unsigned long long seed_lo;
+  long long seed_hi;
+  int32_t* out_entry;
+  int32_t* out_count;
+};
+
+// _prefer(a, b) == a for caller entries a != b (policy.py:88-97)
+__device__ __forceinline__ bool prefer_a(const DevTables& tb, int base, int a, int b) {
+  const double ta = tb.e_thr[base + a], tb_ = tb.e_thr[base + b];
+  if (ta != tb_) return ta > tb_;
+  const double pa = tb.e_pw[base + a], pb = tb.e_pw[base + b];
+  if (pa != pb) return pa < pb;
+  if (tb.e_mtl[base + a] != tb.e_mtl[base + b]) return tb.e_mtl[base + a] < tb.e_mtl[base + b];
+  return tb.e_bs[base + a] <= tb.e_bs[base + b];
+}
+
+__global__ void __launch_bounds__(128) sampling_kernel(const __grid_constant__ SampleParams P) {
+  const DevTables& tb = P.tb;
+  const int g = P.g;
+  const int base = tb.e_off[g];
+  const int64_t total = P.T * P.S;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = q / P.S, i = q - t * P.S;
+    const double cap = P.caps[t * P.ld + i];
+    const uint32_t u = bin_f64((uint64_t)__double_as_longlong(cap), tb.lv.lo, tb.lv.hi, tb.lv.shift1, tb.lv.kbase,
+                               tb.lv.sub0, tb.lv.lut, tb.lv.thr64);
+    const int r = tb.M > 1 ? (int)tb.umap[(size_t)g * tb.U + u] : (int)u;
+    const int n = tb.ccnt[(size_t)g * tb.maxB + r];
+    int cur = -1;
+    if (n > 0 && P.budget >= n) {
+      cur = tb.sel[((size_t)g * 3 + 2) * tb.maxB + r];
+    } else if (n > 0) {
+      // random.Random(seed_base + i): init_by_array key = 32-bit words of abs(seed)
+      __int128 v = (__int128)(((unsigned __int128)(unsigned long long)P.seed_hi << 64) | P.seed_lo) + (__int128)i;
+      unsigned __int128 a = v < 0 ? (unsigned __int128)(-v) : (unsigned __int128)v;
+      uint32_t key[4];
+      int kl = 0;
+      do {
+        key[kl++] = (uint32_t)a;
+        a >>= 32;
+      } while (a && kl < 4);
+      MtLazy rng;
+      mt_lazy_seed(rng, key, kl);
+      const int k = (int)P.budget;
+      const int* cs = tb.csort + base;
+      int best = -1;
+      double best_thr = 0.0;
+      auto consider = [&](int pos) {
+        const double th = tb.e_thr[base + cs[pos]];
+        if (best < 0 || th > best_thr || (th == best_thr && pos < best)) best = pos, best_thr = th;
+      };
+      int32_t slot[kMaxBudget], sval[kMaxBudget];
+      int ns = 0;
+      if ((int64_t)n <= P.setsize) {
+        // pool branch: pool[j] read / pool[j] = pool[n-i-1]; only overwritten slots are stored
+        for (int s = 0; s < k; ++s) {
+          const int j = (int)mt_randbelow(rng, (uint32_t)(n - s));
+          const int last = n - s - 1;
+          int val = j, lval = last, jslot = -1;
+          for (int z = 0; z < ns; ++z) {
+            if (slot[z] == j) val = sval[z], jslot = z;
+            if (slot[z] == last) lval = sval[z];
+          }
+          consider(val);
+          if (jslot < 0) jslot = ns++, slot[jslot] = j;
+          sval[jslot] = lval;
+        }
+      } else {
+        // set branch: redraw until a position not yet selected
+        for (int s = 0; s < k; ++s) {
+          int j;
+          bool dup;
+          do {
+            j = (int)mt_randbelow(rng, (uint32_t)n);
+            dup = false;
+            for (int z = 0; z < ns; ++z) dup |= slot[z] == j;
+          } while (dup);
+          slot[ns++] = j;
+          consider(j);
+        }
+      }
+      cur = cs[best];
+      // hill climb: best feasible strictly-better present neighbour, until none (policy.py:255-266)
+      for (int64_t rr = 0; rr < P.rounds; ++rr) {
+        const int* nb = tb.nbr + (size_t)(base + cur) * 4;
+        const double cthr = tb.e_thr[base + cur];
+        int move = -1;
+        for (int z = 0; z < 4; ++z) {
+          const int e = nb[z];
+          if (e < 0) break;
+          if (tb.e_pw[base + e] > cap || tb.e_thr[base + e] <= cthr) continue;
+          if (move < 0 || !prefer_a(tb, base, move, e)) move = e;
+        }
+        if (move < 0) break;
+        cur = move;
+      }
+    }
+    P.out_entry[q] = cur;
+    if (P.out_count) P.out_count[q] = n;
+  }
+}
+
+}  // namespace
+
+void set_last_launches(int n);
+
+// Random.sample's table-size rule (Lib/random.py): 21, plus 4 ** ceil(log(3k, 4)) when k > 5.
+// 3k is never a power of 4, so the smallest power of 4 >= 3k is exactly that ceiling.
+int64_t sample_setsize(int64_t k) {
+  int64_t s = 21;
+  if (k > 5) {
+    int64_t p = 1;
+    while (p < 3 * k) p *= 4;
+    s += p;
+  }
+  return s;
+}
+
+std::string launch_sampling(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld,
+                            int64_t budget, int64_t rounds, unsigned long long seed_lo, long long seed_hi,
+                            int32_t* out_entry, int32_t* out_count, int sm_count, cudaStream_t st) {
+  if (T <= 0 || S <= 0) return std::string();
+  SampleParams P;
+  P.tb = v;
+  P.g = g;
+  P.caps = caps;
+  P.T = T;
+  P.S = S;
+  P.ld = ld;
+  P.budget = budget;
+  P.rounds = rounds;
+  P.setsize = sample_setsize(budget < kMaxBudget ? budget : kMaxBudget);
+  P.seed_lo = seed_lo;
+  P.seed_hi = seed_hi;
+  P.out_entry = out_entry;
+  P.out_count = out_count;
+  const int threads = 128;
+  const int64_t want = (T * S + threads - 1) / threads;
+  const int64_t cap_blocks = (int64_t)sm_count * 16;
+  sampling_kernel<<<(unsigned)(want < cap_blocks ? want : cap_blocks), threads, 0, st>>>(P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e);
+  set_last_launches(1);
+  return std::string();
+}
+
+}  // namespace cs

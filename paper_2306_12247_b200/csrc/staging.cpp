@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <map>
 #include <set>
 #include <utility>
 
@@ -259,6 +260,50 @@ std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap
         uint64_t k = f32 ? (uint64_t)f32_bits(roundup_f32(t.spw[o])) : f64_bits(t.spw[o]);
         t.vio[u] = std::max(t.vio[u], k);
       }
+    }
+  }
+
+  // ---- sampling selector tables (policy.py:191-273): the combination order (= the sorted
+  // feasible list, policy.py:246), the combination count per grid bin, and each entry's
+  // present-entry neighbourhood (policy.py:200-215: mtl -/+ 1 at the same bs, then the nearest
+  // present bs to bs/2 and bs*2 at the same mtl, ties to the smaller bs).
+  t.csort.clear();
+  t.nbr.clear();
+  t.ccnt.assign((size_t)n_grids * maxB, 0);
+  for (int g = 0; g < n_grids; ++g) {
+    for (const Entry& e : sorted[g]) t.csort.push_back(e.idx);
+    for (int b = 0; b < maxB; ++b) t.ccnt[(size_t)g * maxB + b] = (int32_t)t.cnt[((size_t)g * 3 + 2) * maxB + b];
+    const cs_grid_desc& d = grids[g];
+    std::map<std::pair<int32_t, int32_t>, int32_t> at;
+    std::map<int32_t, std::vector<int32_t>> bs_at;
+    for (int i = 0; i < d.n_entries; ++i) {
+      at[{d.mtl[i], d.bs[i]}] = i;
+      bs_at[d.mtl[i]].push_back(d.bs[i]);
+    }
+    auto find = [&](int32_t m, int32_t b) {
+      auto it = at.find({m, b});
+      return it == at.end() ? -1 : it->second;
+    };
+    for (int i = 0; i < d.n_entries; ++i) {
+      int32_t nb[4] = {-1, -1, -1, -1};
+      int k = 0;
+      for (int32_t m : {d.mtl[i] - 1, d.mtl[i] + 1}) {
+        const int e = m >= 1 ? find(m, d.bs[i]) : -1;
+        if (e >= 0) nb[k++] = e;
+      }
+      for (double target : {(double)d.bs[i] / 2.0, (double)d.bs[i] * 2.0}) {
+        int32_t best = -1;
+        double bd = 0.0;
+        for (int32_t b : bs_at[d.mtl[i]]) {
+          if (b == d.bs[i]) continue;
+          const double dist = std::fabs((double)b - target);
+          if (best < 0 || dist < bd || (dist == bd && b < best)) best = b, bd = dist;
+        }
+        if (best < 0) continue;
+        const int e = find(d.mtl[i], best);
+        if (e >= 0 && std::find(nb, nb + k, e) == nb + k) nb[k++] = e;
+      }
+      t.nbr.insert(t.nbr.end(), nb, nb + 4);
     }
   }
 

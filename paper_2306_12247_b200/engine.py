@@ -211,6 +211,32 @@ class Tables:
                                            cnt.data_ptr(), C.c_void_p(_stream_ptr(None))))
         return sel, cnt
 
+    def select_sampling(self, grid_index: int, caps_dev, n_steps: int, budget_m: int, rounds_r: int,
+                        seed_base: int) -> tuple:
+        """select_sampling at every (trace, step) of an fp64 [T, ld] cap matrix; step i draws with
+        random.Random(seed_base + i) (policy.py:218-273, sim.py:159-163). One thread per step.
+        Returns (entry int32 [T, n_steps] caller index or -1, feasible_count int32 [T, n_steps])."""
+        torch = _torch()
+        if self.cap_dtype != "f64":
+            raise ValueError("select_sampling needs tables staged for fp64 caps")
+        t = caps_dev.shape[0] if caps_dev.dim() == 2 else 1
+        ld = caps_dev.shape[-1]
+        lo_v, hi_v = int(seed_base), int(seed_base) + max(int(n_steps) - 1, 0)
+        if lo_v < -(1 << 127) or hi_v >= (1 << 127):
+            raise NotImplementedError("sampling seeds beyond 127 bits are not supported")
+        two = int(seed_base) & ((1 << 128) - 1)
+        seed_lo = two & ((1 << 64) - 1)
+        seed_hi = two >> 64
+        if seed_hi >= 1 << 63:
+            seed_hi -= 1 << 64
+        ent = torch.empty((t, n_steps), dtype=torch.int32, device=caps_dev.device)
+        cnt = torch.empty((t, n_steps), dtype=torch.int32, device=caps_dev.device)
+        with torch.cuda.device(caps_dev.device):
+            N.check(N.lib().cs_select_sampling(self._h, grid_index, caps_dev.data_ptr(), t, n_steps, ld,
+                                               int(budget_m), int(rounds_r), seed_lo, seed_hi, ent.data_ptr(),
+                                               cnt.data_ptr(), C.c_void_p(_stream_ptr(None))))
+        return ent, cnt
+
     def feasible_caps(self, grid_index: int, policy: int, caps_dev):
         """feasible_set for many caps: warp-per-cap ballot bitmask (policy.py:151-169)."""
         torch = _torch()

@@ -8,8 +8,8 @@ Same names, signatures, result records and error behaviour as the reference
 * ``select_config`` is a warp-per-cap argmax kernel over the regime's entries (shuffles);
 * ``feasible_set`` is a warp-per-cap ballot kernel.
 
-The sampling selector (policy.py:191-273) is outside the accelerated path: ``sampling_policy``
-builds the PolicyKind so reports round-trip, but selecting with it raises NotImplementedError.
+* ``select_sampling`` / ``sampling_steps`` run the sampling kernel, one thread per step, with
+  CPython's random.Random replayed bit for bit (policy.py:191-273).
 """
 
 from __future__ import annotations
@@ -62,7 +62,7 @@ class PolicyKind:
     def index(self) -> int:
         """Position in the engine's policy axis (batching, multi-tenant, combination)."""
         if self.tag is PolicyTag.SAMPLING:
-            raise NotImplementedError("the sampling selector is outside the accelerated path")
+            raise ValueError("sampling is not an exhaustive policy; it has no slot on the policy axis")
         return _POLICY_INDEX[self.tag]
 
 
@@ -224,8 +224,54 @@ def feasible_set(grid: ProfileGrid, kind: PolicyKind, cap_w: float, *, batching_
 
 
 def select_sampling(grid: ProfileGrid, budget_m: int, rounds_r: int, cap_w: float, seed: int) -> Selection:
-    """The sampling selector (policy.py:219-273) is not part of the accelerated path."""
-    raise NotImplementedError("select_sampling is outside the accelerated path of this engine")
+    """Low-overhead selection (policy.py:218-273): probe ``budget_m`` feasible configs drawn by
+    random.Random(seed).sample, then hill-climb ``rounds_r`` rounds over present neighbours,
+    accepting only feasible strictly-better moves. Runs the sampling kernel (one thread)."""
+    return sampling_steps(grid, budget_m, rounds_r, [cap_w], seed)[0]
+
+
+def sampling_steps(grid: ProfileGrid, budget_m: int, rounds_r: int, caps: Sequence[float],
+                   seed_base: int) -> list[Selection]:
+    """select_sampling for a sequence of caps, step i seeded with ``seed_base + i`` (the per-step
+    seeds simulate() uses with seed_base = seed * 1_000_003, sim.py:33-35,159-163). One GPU
+    thread per step."""
+    from .engine import Tables, _torch, require_device
+
+    if budget_m < 1:
+        raise ValueError(f"budget_m must be >= 1, got {budget_m}")
+    if rounds_r < 0:
+        raise ValueError(f"rounds_r must be >= 0, got {rounds_r}")
+    caps = [float(c) for c in caps]
+    for c in caps:
+        _check_cap(c)
+    if not caps:
+        return []
+    torch = _torch()
+    dev = require_device()
+    tables = Tables.for_grid(grid, "f64")
+    # a NaN cap admits nothing (power <= nan is False): the idle bin
+    host = torch.tensor([0.0 if c != c else c for c in caps], dtype=torch.float64).reshape(1, -1)
+    ent, cnt = tables.select_sampling(0, host.to(dev), len(caps), budget_m, rounds_r, seed_base)
+    return decode_entries(grid, ent[0].cpu().numpy(), cnt[0].cpu().numpy())
+
+
+def decode_entries(grid: ProfileGrid, entries: np.ndarray, counts: np.ndarray) -> list[Selection]:
+    """Caller entry indices (-1 idle) + feasible counts -> Selections (shared per distinct pair)."""
+    cfgs = grid.columns()[0]
+    memo: dict = {}
+    out = []
+    for s, c in zip(entries.tolist(), counts.tolist()):
+        sel = memo.get((s, c))
+        if sel is None:
+            if s < 0:
+                sel = IDLE_SELECTION
+            else:
+                e = grid.entries[cfgs[s]]
+                sel = Selection(config=e.config, throughput_ips=e.throughput_ips, power_w=e.power_w,
+                                feasible_count=c)
+            memo[(s, c)] = sel
+        out.append(sel)
+    return out
 
 
 def improvement_pct(a: float, b: float) -> float:

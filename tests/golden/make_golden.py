@@ -13,6 +13,8 @@ Vector sets (reference file:line they pin):
   policy_golden.json  PolicyIndex.select / select_config / feasible_set   policy.py:110-188
   sim_golden.json     simulate + _aggregate (+ slice_report, compare)      sim.py:104-252
   synth_golden.json   synthesize_grid                                      profile.py:169-215
+  controller_golden.json  controller.replay                                controller.py:96-231
+  sampling_golden.json    select_sampling + simulate(sampling_policy)      policy.py:191-273, sim.py:159-163
 """
 
 from __future__ import annotations
@@ -333,10 +335,67 @@ def controller_golden() -> dict:
     return {"source": "capsim 0.1.0 reference, controller.py:96-231", "cases": docs}
 
 
+def sampling_golden() -> dict:
+    """select_sampling (policy.py:218-273) incl. both random.sample branches (pool: n <= setsize,
+    set: n > setsize), the hill climb, and simulate() with a sampling policy (sim.py:159-163)."""
+    from capsim.policy import sampling_policy, select_sampling
+
+    rng = random.Random(31337)
+    g1 = build(G1_POINTS)
+    chain = build({(1, 1): (100.0, 100.0), (1, 2): (200.0, 120.0), (1, 4): (300.0, 140.0), (1, 8): (400.0, 160.0)})
+    sg = synthesize_grid(SynthParams(mtl_cap=4, bs_cap=128, model_name="mobilenet-v1"))
+    seeds = [0, 1, 7, 12345, -5, 2**31 - 1, 2**32, 2**40 + 1, 2**70 + 3, -(2**33) - 9]
+    cases = []
+
+    def add(name, grid, caps, budgets, rounds, seed_list):
+        sels = []
+        for cap in caps:
+            for b in budgets:
+                for r in rounds:
+                    for sd in seed_list:
+                        sels.append([cap, b, r, sd, sel_doc_count(select_sampling(grid, b, r, cap, sd))])
+        cases.append({"name": name, "grid": grid_doc(grid), "queries": sels})
+
+    add("g1", g1, [0.0, 50.0, 100.0, 150.0, 200.0, 250.0, 350.0], [1, 2, 4, 10], [0, 1, 3], seeds[:6])
+    add("chain", chain, [0.0, 130.0, 200.0], [1, 2], [0, 1, 3], seeds)
+    for i in range(30):
+        grid = random_grid(rng, tie_heavy=(i % 3 == 0))
+        caps = boundary_caps(grid, rng, 2)[:10]
+        add(f"rand{i}", grid, caps, [1, 2, 3, 6, rng.randint(7, 40)], [0, 1, 4], [rng.choice(seeds), i])
+    caps = [0.0, 61.0, 100.0, 150.0, 200.0, 260.0, 300.0, 349.0, 350.0]
+    add("synth512", sg, caps, [1, 5, 6, 8, 50, 200, 511, 600], [0, 2, 8], [3, -(2**33) - 9])
+
+    runs = []
+    sim_cases = [
+        ("g1_caps", g1, [200.0, 100.0, 250.0, 0.0, 180.0, 300.0], [(2, 1), (1, 0), (4, 3)], [0, 5], [0.0, 1800.0]),
+        ("synth_day", sg, [rng.uniform(0.0, 350.0) for _ in range(96)], [(1, 0), (4, 2), (30, 1)], [0, -3, 2**40],
+         [0.0, 600.0]),
+    ]
+    for name, grid, vals, kinds, sds, pens in sim_cases:
+        trace = PowerTrace(source_label=name, step_seconds=3600, start_time=T0, values=tuple(vals))
+        for b, r in kinds:
+            for sd in sds:
+                for pen in pens:
+                    rep = simulate(grid, trace, sampling_policy(b, r), seed=sd, switch_penalty_s=pen)
+                    runs.append({"name": name, "budget_m": b, "rounds_r": r, "seed": sd, "switch_penalty_s": pen,
+                                 **report_doc(rep, True)})
+    return {"source": "capsim 0.1.0 reference, policy.py:191-273 + sim.py:159-163", "cases": cases,
+            "sim": {"grids": {"g1_caps": grid_doc(g1), "synth_day": grid_doc(sg)},
+                    "traces": {n: v for n, _, v, *_ in sim_cases}, "runs": runs}}
+
+
+def sel_doc_count(sel) -> list:
+    """Like sel_doc, but idle keeps its feasible_count (always 0) so the record is never null."""
+    if sel.config is None:
+        return [0, 0, 0.0, 0.0, sel.feasible_count]
+    return sel_doc(sel)
+
+
 def main() -> None:
     print("reference capsim from", capsim.__file__)
     for name, fn in (("policy_golden.json", policy_golden), ("sim_golden.json", sim_golden),
-                     ("synth_golden.json", synth_golden), ("controller_golden.json", controller_golden)):
+                     ("synth_golden.json", synth_golden), ("controller_golden.json", controller_golden),
+                     ("sampling_golden.json", sampling_golden)):
         doc = fn()
         (OUT / name).write_text(json.dumps(doc, separators=(",", ":")) + "\n")
         print("wrote", name, (OUT / name).stat().st_size, "bytes")
