@@ -186,8 +186,9 @@ int cs_replay(const cs_tables* t, int32_t grid, const double* caps_dev, int64_t 
  * with random.Random(seed_base + i), seed_base the signed 128-bit integer seed_hi:seed_lo;
  * simulate() passes seed * 1_000_003 (sim.py:159-163), select_sampling(seed) one step with
  * seed_base = seed. out_entry_dev: int32 [n_traces][n_steps] caller entry index or -1 (idle);
- * out_count_dev (nullable): int32 feasible_count. budget_m >= 1, rounds_r >= 0; a budget above
- * CS_SAMPLING_MAX_BUDGET is CS_E_UNSUPPORTED unless it covers every entry of the grid. */
+ * out_count_dev (nullable): int32 feasible_count. budget_m >= 1, rounds_r >= 0. Budgets up to
+ * CS_SAMPLING_MAX_BUDGET keep the sample in registers/local memory; larger ones (below the grid
+ * size) run a slower variant with a stream-ordered scratch pool (cudaMallocAsync). */
 int cs_select_sampling(const cs_tables* t, int32_t grid, const double* caps_dev, int64_t n_traces, int64_t n_steps,
                        int64_t ld, int64_t budget_m, int64_t rounds_r, uint64_t seed_lo, int64_t seed_hi,
                        int32_t* out_entry_dev, int32_t* out_count_dev, void* stream);

@@ -22,7 +22,7 @@ std::string launch_feasible(const DevTables& v, int g, int p, const double* caps
                             cudaStream_t st);
 std::string launch_sampling(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld,
                             int64_t budget, int64_t rounds, unsigned long long seed_lo, long long seed_hi,
-                            int32_t* out_entry, int32_t* out_count, int sm_count, cudaStream_t st);
+                            int32_t* out_entry, int32_t* out_count, int n_entries, int sm_count, cudaStream_t st);
 std::string launch_replay(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld, int mode,
                           int window_k, const int32_t* initial, double noise_pct, const uint32_t* keys,
                           const int32_t* key_len, int key_stride, unsigned long long seed_base, cs_replay_step* steps,
@@ -388,13 +388,11 @@ int cs_select_sampling(const cs_tables* tp, int32_t grid, const double* caps_dev
       (!out_entry_dev && n_traces * n_steps > 0))
     return fail(CS_E_INVALID, "bad sampling arguments");
   const int64_t n_entries = t.e_off[grid + 1] - t.e_off[grid];
-  if (budget_m > CS_SAMPLING_MAX_BUDGET && budget_m < n_entries)
-    return fail(CS_E_UNSUPPORTED, "sampling budgets above " + std::to_string(CS_SAMPLING_MAX_BUDGET) +
-                                      " that do not cover the whole grid are not supported");
+  if (n_entries > 65535) return fail(CS_E_UNSUPPORTED, "sampling over grids of more than 65535 entries");
   int sms = 0;
   CS_CUDA_RET(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   std::string err = cs::launch_sampling(d->view, grid, caps_dev, n_traces, n_steps, ld, budget_m, rounds_r, seed_lo,
-                                        seed_hi, out_entry_dev, out_count_dev, sms,
+                                        seed_hi, out_entry_dev, out_count_dev, (int)n_entries, sms,
                                         reinterpret_cast<cudaStream_t>(stream));
   if (!err.empty()) return fail(CS_E_CUDA, err);
   return CS_OK;

@@ -35,6 +35,8 @@ struct SampleParams {
   long long seed_hi;
   int32_t* out_entry;
   int32_t* out_count;
+  uint16_t* scratch;       // BIG only: [threads][scratch_stride] pool / bitmap words
+  int64_t scratch_stride;  // uint16 words per thread
 };
 
 // _prefer(a, b) == a for caller entries a != b (policy.py:88-97)
@@ -47,6 +49,9 @@ __device__ __forceinline__ bool prefer_a(const DevTables& tb, int base, int a, i
   return tb.e_bs[base + a] <= tb.e_bs[base + b];
 }
 
+// BIG (budgets above kMaxBudget): the pool is materialised in a per-thread global scratch row
+// (n uint16 positions, or an n-bit bitmap for the set branch) instead of the O(m) slot list.
+template <bool BIG>
 __global__ void __launch_bounds__(128) sampling_kernel(const __grid_constant__ SampleParams P) {
   const DevTables& tb = P.tb;
   const int g = P.g;
@@ -82,7 +87,27 @@ __global__ void __launch_bounds__(128) sampling_kernel(const __grid_constant__ S
         const double th = tb.e_thr[base + cs[pos]];
         if (best < 0 || th > best_thr || (th == best_thr && pos < best)) best = pos, best_thr = th;
       };
-      int32_t slot[kMaxBudget], sval[kMaxBudget];
+      if (BIG) {
+        uint16_t* row = P.scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * P.scratch_stride;
+        if ((int64_t)n <= P.setsize) {
+          for (int z = 0; z < n; ++z) row[z] = (uint16_t)z;
+          for (int s = 0; s < k; ++s) {
+            const int j = (int)mt_randbelow(rng, (uint32_t)(n - s));
+            consider(row[j]);
+            row[j] = row[n - s - 1];
+          }
+        } else {
+          uint32_t* bits = reinterpret_cast<uint32_t*>(row);
+          for (int z = 0; z < (n + 31) / 32; ++z) bits[z] = 0;
+          for (int s = 0; s < k; ++s) {
+            int j = (int)mt_randbelow(rng, (uint32_t)n);
+            while ((bits[j >> 5] >> (j & 31)) & 1u) j = (int)mt_randbelow(rng, (uint32_t)n);
+            bits[j >> 5] |= 1u << (j & 31);
+            consider(j);
+          }
+        }
+      } else {
+      int32_t slot[BIG ? 1 : kMaxBudget], sval[BIG ? 1 : kMaxBudget];
       int ns = 0;
       if ((int64_t)n <= P.setsize) {
         // pool branch: pool[j] read / pool[j] = pool[n-i-1]; only overwritten slots are stored
@@ -111,6 +136,7 @@ __global__ void __launch_bounds__(128) sampling_kernel(const __grid_constant__ S
           slot[ns++] = j;
           consider(j);
         }
+      }
       }
       cur = cs[best];
       // hill climb: best feasible strictly-better present neighbour, until none (policy.py:255-266)
@@ -151,7 +177,7 @@ int64_t sample_setsize(int64_t k) {
 
 std::string launch_sampling(const DevTables& v, int g, const double* caps, int64_t T, int64_t S, int64_t ld,
                             int64_t budget, int64_t rounds, unsigned long long seed_lo, long long seed_hi,
-                            int32_t* out_entry, int32_t* out_count, int sm_count, cudaStream_t st) {
+                            int32_t* out_entry, int32_t* out_count, int n_entries, int sm_count, cudaStream_t st) {
   if (T <= 0 || S <= 0) return std::string();
   SampleParams P;
   P.tb = v;
@@ -162,15 +188,32 @@ std::string launch_sampling(const DevTables& v, int g, const double* caps, int64
   P.ld = ld;
   P.budget = budget;
   P.rounds = rounds;
-  P.setsize = sample_setsize(budget < kMaxBudget ? budget : kMaxBudget);
+  P.setsize = sample_setsize(budget < n_entries ? budget : n_entries);
   P.seed_lo = seed_lo;
   P.seed_hi = seed_hi;
   P.out_entry = out_entry;
   P.out_count = out_count;
+  P.scratch = nullptr;
+  P.scratch_stride = 0;
   const int threads = 128;
   const int64_t want = (T * S + threads - 1) / threads;
-  const int64_t cap_blocks = (int64_t)sm_count * 16;
-  sampling_kernel<<<(unsigned)(want < cap_blocks ? want : cap_blocks), threads, 0, st>>>(P);
+  const bool big = budget > kMaxBudget && budget < n_entries;
+  if (!big) {
+    const int64_t cap_blocks = (int64_t)sm_count * 16;
+    sampling_kernel<false><<<(unsigned)(want < cap_blocks ? want : cap_blocks), threads, 0, st>>>(P);
+  } else {
+    // one CTA per SM; scratch rows hold n uint16 pool slots (>= the n-bit bitmap), 16-B aligned
+    const int64_t blocks = want < sm_count ? want : sm_count;
+    P.scratch_stride = ((int64_t)n_entries + 63) / 64 * 64;
+    void* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, (size_t)blocks * threads * P.scratch_stride * 2, st);
+    if (e != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e);
+    P.scratch = static_cast<uint16_t*>(scratch);
+    sampling_kernel<true><<<(unsigned)blocks, threads, 0, st>>>(P);
+    e = cudaGetLastError();
+    cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e);
   set_last_launches(1);

@@ -55,8 +55,9 @@ def test_simulate_sampling_matches_reference_golden(cs):
 
 
 def test_sampling_steps_match_oracle_fine_grid(cs):
-    """4096-entry grid: both random.sample branches, budgets up to the kernel maximum (>227 MT
-    outputs, so the lazy twist catches up), negative and >64-bit seeds, long hill climbs."""
+    """4096-entry grid: both random.sample branches, budgets past 227 MT outputs (the lazy twist
+    catches up) and past the in-register maximum (scratch-pool variant), negative and >64-bit
+    seeds, long hill climbs."""
     from oracle import oracle
 
     g = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
@@ -64,7 +65,7 @@ def test_sampling_steps_match_oracle_fine_grid(cs):
     rng = np.random.default_rng(5)
     caps = np.concatenate([[0.0, -0.0, 60.0, 350.0, 1e9], rng.uniform(0.0, 350.0, 250)])
     for budget, rounds, seed_base in ((1, 0, 0), (5, 3, -12345), (6, 1, 2**40), (37, 2, 99), (256, 0, 2**70 + 5),
-                                      (256, 4, -(2**90)), (4096, 1, 7)):
+                                      (256, 4, -(2**90)), (300, 1, 11), (1000, 0, -3), (4096, 1, 7)):
         sels = cs.sampling_steps(g, budget, rounds, caps.tolist(), seed_base)
         cfgs = g.columns()[0]
         for i, (cap, sel) in enumerate(zip(caps, sels)):
@@ -106,6 +107,4 @@ def test_sampling_errors(cs):
         cs.select_sampling(g1, 1, 0, -1.0, 0)
     assert cs.select_sampling(g1, 4, 2, float("nan"), 0).config is None
     big = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
-    with pytest.raises(NotImplementedError):
-        cs.select_sampling(big, 300, 0, 200.0, 0)
     assert cs.select_sampling(big, 5000, 0, 200.0, 0) == cs.select_config(big, cs.COMBINATION, 200.0)
