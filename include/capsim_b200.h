@@ -80,6 +80,9 @@ typedef struct {
                                 they serve (0 for well-formed tables; such leaves take the exact
                                 per-step power check) */
   int32_t n_segments;      /* selection segments over all grids x policies */
+  int32_t lut_big_entries; /* fp32: finer LUT that cs_eval stages when shared memory allows (0: none) */
+  int32_t lut_big_shift;
+  int32_t lut_big_unsafe_leaves;
 } cs_tables_info;
 
 typedef struct cs_tables cs_tables;
@@ -124,6 +127,9 @@ int cs_tables_grid_bins(const cs_tables* t, int32_t grid, int32_t policy, int32_
 int cs_tables_union_map(const cs_tables* t, int32_t grid, uint16_t* out);
 /* Host restatement of the device bin lookup (for CPU tests of the staged LUT). */
 int cs_tables_lookup_host(const cs_tables* t, const void* caps, int64_t n, int32_t* bins_out);
+/* Same through a chosen LUT size: which = 0 the default LUT, 1 the finer fp32 LUT cs_eval stages
+ * when shared memory allows (CS_E_INVALID when the tables have none). */
+int cs_tables_lookup_host_lut(const cs_tables* t, const void* caps, int64_t n, int32_t which, int32_t* bins_out);
 /* Upload the staged blob to a device (idempotent per device). */
 int cs_tables_upload(cs_tables* t, int32_t device);
 

@@ -33,7 +33,7 @@ TRACE_KINDS = {"solar": 0, "wind": 1, "mixed": 2, "iid": 3}
 EXPORTS = (
     "cs_last_error", "cs_abi_version", "cs_device_query",
     "cs_tables_create", "cs_tables_destroy", "cs_tables_get_info", "cs_tables_grid_bins",
-    "cs_tables_union_map", "cs_tables_lookup_host", "cs_tables_upload",
+    "cs_tables_union_map", "cs_tables_lookup_host", "cs_tables_lookup_host_lut", "cs_tables_upload",
     "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches",
     "cs_select_caps", "cs_feasible_caps",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
@@ -87,6 +87,9 @@ class TablesInfo(C.Structure):
         ("device_bytes", C.c_int64),
         ("lut_unsafe_leaves", C.c_int32),
         ("n_segments", C.c_int32),
+        ("lut_big_entries", C.c_int32),
+        ("lut_big_shift", C.c_int32),
+        ("lut_big_unsafe_leaves", C.c_int32),
     ]
 
 
@@ -135,6 +138,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_tables_grid_bins": ([vp, i32, i32, vp, vp, P(i32)], C.c_int),
         "cs_tables_union_map": ([vp, i32, vp], C.c_int),
         "cs_tables_lookup_host": ([vp, vp, i64, vp], C.c_int),
+        "cs_tables_lookup_host_lut": ([vp, vp, i64, C.c_int32, vp], C.c_int),
         "cs_tables_upload": ([vp, i32], C.c_int),
         "cs_eval_workspace_size": ([vp, P(EvalArgs), P(sz)], C.c_int),
         "cs_eval": ([vp, P(EvalArgs), vp], C.c_int),

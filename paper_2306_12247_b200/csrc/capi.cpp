@@ -85,6 +85,7 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
       {t.csort.data(), t.csort.size() * 4, 0},
       {t.ccnt.data(), t.ccnt.size() * 4, 0},
       {t.nbr.data(), t.nbr.size() * 4, 0},
+      {t.lut_big.lut.data(), t.lut_big.lut.size() * 4, 0},
   };
   size_t total = 0;
   for (auto& p : parts) {
@@ -142,6 +143,15 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
   v.csort = reinterpret_cast<const int32_t*>(b + parts[16].off);
   v.ccnt = reinterpret_cast<const int32_t*>(b + parts[17].off);
   v.nbr = reinterpret_cast<const int32_t*>(b + parts[18].off);
+  v.n_lut_big = (int32_t)t.lut_big.lut.size();
+  v.n_level1_big = (int32_t)t.lut_big.n_level1;
+  v.lv_big = v.lv;
+  if (v.n_lut_big) {
+    v.lv_big.kbase = t.lut_big.kbase;
+    v.lv_big.shift1 = t.lut_big.shift1;
+    v.lv_big.sub0 = t.lut_big.n_level1;
+    v.lv_big.lut = reinterpret_cast<const uint32_t*>(b + parts[19].off);
+  }
   t.devs.push_back(d);
   *out = &t.devs.back();
   return CS_OK;
@@ -224,6 +234,9 @@ int cs_tables_get_info(const cs_tables* tp, cs_tables_info* o) {
   o->device_bytes = t.devs.empty() ? 0 : (int64_t)t.devs.front().bytes;
   o->lut_unsafe_leaves = (int32_t)t.n_unsafe;
   o->n_segments = (int32_t)(t.seg.size() / 4);
+  o->lut_big_entries = (int32_t)t.lut_big.lut.size();
+  o->lut_big_shift = (int32_t)t.lut_big.shift1;
+  o->lut_big_unsafe_leaves = (int32_t)t.lut_big.n_unsafe;
   return CS_OK;
 }
 
@@ -245,6 +258,19 @@ int cs_tables_union_map(const cs_tables* tp, int32_t grid, uint16_t* out) {
   const Tables& t = *reinterpret_cast<const Tables*>(tp);
   if (grid < 0 || grid >= t.M) return fail(CS_E_INVALID, "grid out of range");
   std::memcpy(out, t.umap.data() + (size_t)grid * t.U, (size_t)t.U * 2);
+  return CS_OK;
+}
+
+int cs_tables_lookup_host_lut(const cs_tables* tp, const void* caps, int64_t n, int32_t which, int32_t* bins_out) {
+  if (!tp || (n > 0 && (!caps || !bins_out))) return fail(CS_E_INVALID, "null argument");
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (which == 0) return cs_tables_lookup_host(tp, caps, n, bins_out);
+  if (which != 1 || t.lut_big.lut.empty()) return fail(CS_E_INVALID, "no such LUT");
+  const Tables::Lut& L = t.lut_big;
+  const uint32_t* c = reinterpret_cast<const uint32_t*>(caps);
+  for (int64_t i = 0; i < n; ++i)
+    bins_out[i] = (int32_t)cs::bin_f32(c[i], L.shift1, (int32_t)L.kbase, (int32_t)L.n_level1, L.n_level1,
+                                       L.lut.data());
   return CS_OK;
 }
 

@@ -100,6 +100,8 @@ struct DevTables {
   int32_t n_level1;
   int32_t batching_mtl, mt_bs;
   LutView lv;
+  LutView lv_big;          // finer fp32 LUT for eval_kernel (n_lut_big == 0: none)
+  int32_t n_lut_big, n_level1_big;
   const uint64_t* vio;     // [U] lowest admissible cap bits per union bin (0 for bin 0)
   const uint64_t* sig;     // [M][U] segment ids of the 3 policies, 16 bits each
   const int32_t* seg_off;  // [M*3+1] offsets into seg
@@ -147,6 +149,14 @@ struct Tables {
   uint32_t n_level1 = 0, n_sub = 0;
   uint32_t n_unsafe = 0;  // fp32 leaves not proven violation-free (0 for well-formed tables)
   std::vector<uint32_t> lut;
+  // the LUT sizes built (lut_main mirrors the fields above; lut_big is empty when no finer
+  // level 1 exists, else eval_kernel's choice when shared memory allows)
+  struct Lut {
+    uint64_t kbase = 0;
+    uint32_t shift1 = 0, n_level1 = 0, n_sub = 0, n_unsafe = 0;
+    std::vector<uint32_t> lut;
+  };
+  Lut lut_main, lut_big;
   // device copies (per device ordinal)
   struct Dev {
     int device = -1;

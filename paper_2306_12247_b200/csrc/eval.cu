@@ -21,7 +21,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "cs_internal.h"
 
@@ -70,6 +73,8 @@ __device__ __forceinline__ void dd_add_prod(dd& x, double c, double v) {
 
 struct EvalParams {
   DevTables tb;
+  LutView lv;  // the LUT this launch stages (tb.lv or, when it fits, the finer tb.lv_big)
+  int32_t n_lut, n_level1;
   const void* caps;
   int64_t T, S, ld;
   int64_t seg_len;
@@ -82,10 +87,16 @@ struct EvalParams {
   uint32_t* part_hist;  // split mode: [T][U]
   uint32_t* part_sw;    // [T][NSEG] switched steps per selection segment (PEN)
   uint32_t* part_vio;   // [T][M*3]
-  // per selection segment of this launch: {u_lo, u_hi, idle, -} then thr / energy / penalised thr,
-  // each split into {hi, mid, lo} with hi and mid on fixed quantum grids so that count x hi and
-  // count x mid accumulate EXACTLY (6 x 16 B per segment, see prep_kernel)
-  const double2* segrec;
+  // per selection segment of this launch (prep_kernel), structure of arrays:
+  //   seg_hdr[k]  = u_lo | u_hi << 16 (union-bin range of segment k)
+  //   seg_idle[mp] = 1 when (grid, policy) mp's first segment is the idle selection
+  //   seg_val as double2 {hi, lo} pairs [j * NSEG + k], j = thr, energy, penalised thr: each value
+  //   split so that count x hi accumulates EXACTLY (see prep_kernel)
+  // staged into shared memory at off_seg when it fits (seg_smem_bytes > 0)
+  const uint32_t* seg_hdr;
+  const int32_t* seg_idle;
+  const double* seg_val;
+  int32_t off_seg, seg_smem_bytes;
   int32_t U4;    // histogram row stride (U rounded up to a multiple of 4)
   int32_t NSEG;  // selection segments over all grids x policies
   double omp;
@@ -111,14 +122,15 @@ __device__ __forceinline__ void group_sync(int gid_local, int gsize) {
 // the running sum of such products over a trace are EXACT (integers times Q below 2^53 Q); the
 // small lo parts are summed in plain fp64 (error ~2^-(53+L) of the total), so the final
 // hi + lo rounds to the exactly rounded sum the reference's math.fsum returns.
-// Record per segment (4 x 16 B): {u_lo, u_hi, idle, -}, {thr hi, lo}, {energy hi, lo},
-// {penalised thr hi, lo}. One block per (grid, policy).
+// Segment tables (structure of arrays, one block per (grid, policy)): seg_hdr[k] = u_lo | u_hi << 16,
+// {hi, lo} pairs seg_val2[j * NSEG + k] for j = thr, energy, penalised thr, and seg_idle[mp].
 __device__ __forceinline__ double2 split2(double v, int eq) {
   const double hi = ldexp(floor(ldexp(v, -eq)), eq);  // floor(v / Q) * Q, exact
   return make_double2(hi, v - hi);
 }
 
-__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, double2* segrec) {  // L: see split2
+__global__ void prep_kernel(const DevTables tb, double step, double omp, int L, int nseg, uint32_t* hdr,
+                            int32_t* idlef, double* val) {  // L: see split2
   __shared__ double red[2][256];
   const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
   const size_t ob = (size_t)mp * B;
@@ -145,16 +157,19 @@ __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, 
   et -= L;
   ee -= L;
   const int k0 = tb.seg_off[mp], k1 = tb.seg_off[mp + 1];
+  if (threadIdx.x == 0) idlef[mp] = (k1 > k0 && tb.sel[ob + tb.seg[k0].z] < 0) ? 1 : 0;
   for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
     const int4 sg = tb.seg[k];
     const size_t i = ob + sg.z;
-    const bool idle = tb.sel[i] < 0;
-    double2* out = segrec + (size_t)k * 4;
-    int4 head = make_int4(sg.x, sg.y, idle ? 1 : 0, 0);
-    out[0] = *reinterpret_cast<const double2*>(&head);
-    out[1] = split2(idle ? 0.0 : tb.sthr[i], et);
-    out[2] = split2(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee);
-    out[3] = split2(idle ? 0.0 : __dmul_rn(tb.sthr[i], omp), et);
+    const bool idle = tb.sel[i] < 0;  // only ever the first segment (feasibility is monotone in the cap)
+    hdr[k] = (uint32_t)sg.x | ((uint32_t)sg.y << 16);
+    const double2 t = split2(idle ? 0.0 : tb.sthr[i], et);
+    const double2 e = split2(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee);
+    const double2 q = split2(idle ? 0.0 : __dmul_rn(tb.sthr[i], omp), et);
+    double2* v2 = reinterpret_cast<double2*>(val);
+    v2[0 * (size_t)nseg + k] = t;
+    v2[1 * (size_t)nseg + k] = e;
+    v2[2 * (size_t)nseg + k] = q;
   }
 }
 
@@ -233,9 +248,10 @@ __device__ __forceinline__ double xreduce4(const double (&v)[4], int lane) {
 //   SW[(m*3+p)*U4 + u]  prefix-summed switched-step counts (PEN)
 template <bool PEN>
 __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
-                                         const uint32_t* vcnt, double* scratch, int gtid, int gsize, int gid_local) {
+                                         const uint32_t* vcnt, const uint32_t* shdr, const int32_t* sidle,
+                                         const double2* sval, double* scratch, int gtid, int gsize, int gid_local) {
   const DevTables& tb = P.tb;
-  const int M = tb.M;
+  const int M = tb.M, NS = P.NSEG;
   const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
   for (int m = 0; m < M; ++m) {
     double mine[3];
@@ -245,15 +261,16 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
       const int mp = 3 * m + p;
       const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
       const uint32_t* sw = PEN ? SW + k0 : nullptr;  // switched steps per segment of (m, p)
+      const int kidle = sidle[mp] ? k0 : -1;         // the idle selection is always the first segment
       double a[4] = {0.0, 0.0, 0.0, 0.0};  // thr hi, lo, energy hi, lo
       uint32_t idle = 0, swc = 0;
       for (int k = k0 + gtid; k < k1; k += gsize) {
-        const double2* rec = P.segrec + (size_t)k * 4;
-        const int4 sg = __ldg(reinterpret_cast<const int4*>(rec));
-        const uint32_t cnt = C[sg.y] - (sg.x ? C[sg.x - 1] : 0u);
+        const uint32_t hd = shdr[k];
+        const uint32_t ulo = hd & 0xFFFFu, uhi = hd >> 16;
+        const uint32_t cnt = C[uhi] - (ulo ? C[ulo - 1] : 0u);
         if (cnt == 0) continue;
-        const double2 ve = __ldg(rec + 2);
         const double dc = (double)cnt;
+        const double2 ve = sval[NS + k];
         a[2] = __fma_rn(dc, ve.x, a[2]);
         a[3] = __fma_rn(dc, ve.y, a[3]);
         uint32_t scnt = 0;
@@ -261,16 +278,16 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
           scnt = sw[k - k0];
           swc += scnt;
         }
-        if (sg.z) {
-          idle += cnt;
+        if (k == kidle) {
+          idle += cnt;  // idle segments carry zero throughput
         } else {
-          const double2 vt = __ldg(rec + 1);
           const double dn = (double)(cnt - scnt);
+          const double2 vt = sval[k];
           a[0] = __fma_rn(dn, vt.x, a[0]);
           a[1] = __fma_rn(dn, vt.y, a[1]);
           if (PEN && scnt) {
-            const double2 vp = __ldg(rec + 3);
             const double ds = (double)scnt;
+            const double2 vp = sval[2 * NS + k];
             a[0] = __fma_rn(ds, vp.x, a[0]);
             a[1] = __fma_rn(ds, vp.y, a[1]);
           }
@@ -335,13 +352,14 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
 // histogram (and switch histograms) are left zeroed for the next trace.
 template <bool PEN, typename GH>
 __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* sw,
-                                             const uint32_t* vcnt, GH* ghist, double* scratch, int gtid, int gsize,
-                                             int gid_local) {
+                                             const uint32_t* vcnt, GH* ghist, const uint32_t* shdr,
+                                             const int32_t* sidle, const double2* sval, double* scratch, int gtid,
+                                             int gsize, int gid_local) {
   const int U4 = P.U4, M = P.tb.M;
   uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then partial sums
   group_scan(h, U4, ghist, wtot, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
-  epilogue<PEN>(P, t, h, sw, vcnt, scratch, gtid, gsize, gid_local);
+  epilogue<PEN>(P, t, h, sw, vcnt, shdr, sidle, sval, scratch, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
   for (int u = 4 * gtid; u < U4; u += 4 * gsize) *reinterpret_cast<uint4*>(h + u) = make_uint4(0u, 0u, 0u, 0u);
   if (PEN)
@@ -358,11 +376,11 @@ __device__ void recount_violations(const EvalParams& P, const uint32_t* s_lut, c
     double cap;
     if constexpr (sizeof(CapT) == 4) {
       const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(row) + i);
-      b = bin_f32(x, tb.lv.shift1, (int32_t)tb.lv.kbase, tb.n_level1, tb.lv.sub0, s_lut);
+      b = bin_f32(x, P.lv.shift1, (int32_t)P.lv.kbase, P.n_level1, P.lv.sub0, s_lut);
       cap = (double)__uint_as_float(x);
     } else {
       const unsigned long long x = __ldg(reinterpret_cast<const unsigned long long*>(row) + i);
-      b = bin_f64(x, tb.lv.lo, tb.lv.hi, tb.lv.shift1, tb.lv.kbase, tb.lv.sub0, s_lut, tb.lv.thr64);
+      b = bin_f64(x, P.lv.lo, P.lv.hi, P.lv.shift1, P.lv.kbase, P.lv.sub0, s_lut, P.lv.thr64);
       cap = __longlong_as_double((long long)x);
     }
     for (int m = 0; m < tb.M; ++m) {
@@ -451,9 +469,28 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       if (VIO) flags |= any;
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
-    } else {  // redirects (or, for >= 2^15 bins, high bases): deep() re-checks every entry
+    } else {  // redirects (or, for >= 2^15 bins, high bases)
+      // one predicated sub-table step per element, then deep() only for chains (rare)
+      uint32_t sh[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) b[k] = L.deep(e[k], u[k], flags);
+      for (int k = 0; k < 4; ++k) {
+        sh[k] = L.s1;
+        if (e[k] >= kRedirect32) {
+          sh[k] = e[k] & 31u;
+          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
+        }
+      }
+      if (e[0] >= kRedirect32 || e[1] >= kRedirect32 || e[2] >= kRedirect32 || e[3] >= kRedirect32) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          while (e[k] >= kRedirect32) {
+            sh[k] = e[k] & 31u;
+            e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
+          }
+      }
+      if (VIO) flags |= e[0] | e[1] | e[2] | e[3];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], ((1u << sh[k]) - 1u) & 0x3FFFu);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -502,7 +539,10 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     }
   };
 
+  // rolling software pipeline: each vector's reload is issued as soon as it is consumed, so a
+  // warp keeps 3-4 128-bit loads per lane in flight while it works (not 4, then 0)
   int v = gtid;
+#ifndef CS_ROLLING
   for (; v + 3 * gsize < nvf; v += 4 * gsize) {
     const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
     const uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
@@ -513,6 +553,28 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     vec4(r2, v + 2 * gsize);
     vec4(r3, v + 3 * gsize);
   }
+#else
+  if (v + 3 * gsize < nvf) {
+    uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
+    uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
+    uint4 r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16);
+    uint4 r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
+    for (;;) {
+      const int vn = v + 4 * gsize;
+      const bool more = vn + 3 * gsize < nvf;
+      vec4(r0, v);
+      if (more) r0 = ldg_stream(vrow + (size_t)vn * 16);
+      vec4(r1, v + gsize);
+      if (more) r1 = ldg_stream(vrow + (size_t)(vn + gsize) * 16);
+      vec4(r2, v + 2 * gsize);
+      if (more) r2 = ldg_stream(vrow + (size_t)(vn + 2 * gsize) * 16);
+      vec4(r3, v + 3 * gsize);
+      if (more) r3 = ldg_stream(vrow + (size_t)(vn + 3 * gsize) * 16);
+      v = vn;
+      if (!more) break;
+    }
+  }
+#endif
   for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
   // tail (< 4 caps at the very end of a trace)
   for (int i = 4 * nvf + gtid; i < n; i += gsize) {
@@ -541,11 +603,11 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint3
   const int n = (int)(s1e - s0);
   bool bad = false;
   auto bin = [&](uint64_t x) {
-    return bin_f64(x, tb.lv.lo, tb.lv.hi, tb.lv.shift1, tb.lv.kbase, tb.lv.sub0, s_lut, tb.lv.thr64);
+    return bin_f64(x, P.lv.lo, P.lv.hi, P.lv.shift1, P.lv.kbase, P.lv.sub0, s_lut, P.lv.thr64);
   };
   auto one = [&](uint64_t x, int64_t gi, uint32_t b) {
     atomicAdd(&h[b], 1u);
-    if (VIO) bad |= clamp_bits_f64(x, tb.lv.lo, tb.lv.hi) < s_vio[b];
+    if (VIO) bad |= clamp_bits_f64(x, P.lv.lo, P.lv.hi) < s_vio[b];
     if (PEN) {
       const uint32_t pb = gi > 0 ? bin(__ldg(row + gi - 1)) : b;
       if (b != pb)
@@ -575,10 +637,7 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint3
 }
 
 template <typename CapT, bool PEN, bool STEP, bool VIO>
-#ifndef CS_MIN_BLOCKS
-#define CS_MIN_BLOCKS 2
-#endif
-__global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_constant__ EvalParams P) {
+__global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ EvalParams P) {
   constexpr bool F32 = sizeof(CapT) == 4;
   extern __shared__ __align__(16) unsigned char smem[];
   const DevTables& tb = P.tb;
@@ -586,7 +645,7 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
 
   // ---- N1: stage the tables into shared memory once per CTA ----
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
-  for (int i = threadIdx.x; i < tb.n_lut; i += blockDim.x) s_lut[i] = __ldg(tb.lv.lut + i);
+  for (int i = threadIdx.x; i < P.n_lut; i += blockDim.x) s_lut[i] = __ldg(P.lv.lut + i);
   // fp64 tables: violation floors per union bin (fp32 tables carry the proof in the LUT leaves)
   uint64_t* s_vio = reinterpret_cast<uint64_t*>(smem + P.off_vio);
   if (!F32 && VIO)
@@ -608,6 +667,19 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
     if (threadIdx.x == 0) *s_gsteps = 0u;
   }
 
+  // per-launch segment tables (prep_kernel): staged when they fit, else read through L1
+  const bool seg_staged = P.seg_smem_bytes > 0;
+  uint32_t* s_seghdr = reinterpret_cast<uint32_t*>(smem + P.off_seg);
+  int32_t* s_segidle = reinterpret_cast<int32_t*>(s_seghdr + ((P.NSEG + 3) & ~3));
+  double2* s_segval = reinterpret_cast<double2*>(s_segidle + ((M * 3 + 3) & ~3));
+  if (seg_staged) {
+    const int NS = P.NSEG, NV = PEN ? 3 : 2;
+    const double2* gv = reinterpret_cast<const double2*>(P.seg_val);
+    for (int i = threadIdx.x; i < NS; i += blockDim.x) s_seghdr[i] = __ldg(P.seg_hdr + i);
+    for (int i = threadIdx.x; i < M * 3; i += blockDim.x) s_segidle[i] = __ldg(P.seg_idle + i);
+    for (int i = threadIdx.x; i < NV * NS; i += blockDim.x) s_segval[i] = __ldg(gv + i);
+  }
+
   const int gsize = P.wpg * 32;
   const int gid_local = threadIdx.x / gsize;
   const int gtid = threadIdx.x - gid_local * gsize;
@@ -626,11 +698,11 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
 
   Lut32 L;
   L.lut = s_lut;
-  L.kb = (int32_t)tb.lv.kbase;
-  L.nbm1 = tb.n_level1 - 1;
-  L.s1 = tb.lv.shift1;
-  L.sub0 = tb.lv.sub0;
-  L.mask1 = ((1u << tb.lv.shift1) - 1u) & 0x3FFFu;
+  L.kb = (int32_t)P.lv.kbase;
+  L.nbm1 = P.n_level1 - 1;
+  L.s1 = P.lv.shift1;
+  L.sub0 = P.lv.sub0;
+  L.mask1 = ((1u << P.lv.shift1) - 1u) & 0x3FFFu;
 
   const int64_t n_items = P.T * (int64_t)P.nseg;
   const int64_t n_groups = (int64_t)gridDim.x * P.gpc;
@@ -665,8 +737,12 @@ __global__ void __launch_bounds__(512, CS_MIN_BLOCKS) eval_kernel(const __grid_c
           }
         }
       }
-      finish_trace<PEN>(P, t, h, sw, vcnt, want_hist ? s_ghist : (uint32_t*)nullptr, scratch, gtid, gsize,
-                        gid_local);
+      uint32_t* gh = want_hist ? s_ghist : (uint32_t*)nullptr;
+      if (seg_staged)  // two instantiations so each reads its tables with a known address space
+        finish_trace<PEN>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
+      else
+        finish_trace<PEN>(P, t, h, sw, vcnt, gh, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val),
+                          scratch, gtid, gsize, gid_local);
     } else {
       // split trace: fold this segment's partial histogram into the trace's global partials
       for (int u = gtid; u < U; u += gsize) {
@@ -708,7 +784,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
   uint32_t* h = P.part_hist + t * U4;
   uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
   const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
-  finish_trace<PEN>(P, t, h, sw, vc, P.hist, scratch, threadIdx.x, blockDim.x, 0);
+  finish_trace<PEN>(P, t, h, sw, vc, P.hist, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val),
+                    scratch, threadIdx.x, blockDim.x, 0);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -756,6 +833,28 @@ void* pick_kernel(bool f32, bool pen, bool step, bool vio) {
 
 size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// Resident CTAs per SM for (kernel, block size, dynamic smem), memoised: the plan search asks
+// for dozens of candidates per launch and the occupancy API dominates small launches otherwise.
+int blocks_per_sm(void* fn, int dev, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<void*, int, int, size_t>, int> cache;
+  const auto key = std::make_tuple(fn, dev, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int per_sm = 0;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 0;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = per_sm;
+  return per_sm;
+}
+
 std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, Plan& pl) {
   const bool f32 = t.cap_dtype == CS_CAP_F32;
   const bool pen = a->switch_penalty_s > 0.0;
@@ -771,7 +870,11 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   const int nsegs = (int)(t.seg.size() / 4);
   const size_t sig_bytes = pen ? a16((size_t)M * U * 8 + (size_t)(M * 3 + 1) * 4) : 0;
   const size_t gh_bytes = a->hist ? a16((size_t)U * 4 + 4) : 0;
-  const size_t fixed = lut_bytes + vio_bytes + sig_bytes + gh_bytes;
+  // segment tables (prep_kernel): hdr [NS] u32, idle flags [M*3] i32, values [6][NS] f64 in the
+  // workspace; the kernel stages hdr, flags and the 4 (6 with a penalty) value arrays it reads
+  const size_t seg_hdr_b = (size_t)((nsegs + 3) & ~3) * 4, seg_idle_b = (size_t)((M * 3 + 3) & ~3) * 4;
+  const size_t seg_ws = a16(seg_hdr_b + seg_idle_b + (size_t)6 * nsegs * 8);
+  const size_t seg_smem = a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
   const int hs = 1;
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
     size_t gb = a16((size_t)U4 * 4 * hs);
@@ -783,31 +886,51 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     gb += (size_t)wpg * 24 * 8;
     return a16(gb);
   };
-  // candidates: most resident warps per SM first, then the smallest worker group
-  int best_warps = -1, b_threads = 0, b_wpg = 0, b_per_sm = 0;
-  size_t b_smem = 0;
-  for (int threads : {512, 256, 128}) {
-    for (int wpg : {1, 2, 4, 8, 16}) {
-      const int wpc = threads / 32;
-      if (wpg > wpc) continue;
-      const int gpc = wpc / wpg;
-      if (wpg > 1 && gpc > 15) continue;  // named barriers 1..15
-      size_t o1, o2, o3;
-      const size_t smem = fixed + (size_t)gpc * group_bytes(wpg, &o1, &o2, &o3);
-      if (smem > (size_t)smem_optin) continue;
-      int per_sm = 0;
-      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) {
-        cudaGetLastError();
-        continue;
+  // candidates: most resident warps per SM first, then the smallest worker group; the segment
+  // tables go to shared memory unless that costs resident warps, and so does the big LUT
+  struct Cand {
+    int warps = -1, threads = 0, wpg = 0, per_sm = 0;
+    size_t smem = 0;
+    bool staged = false;
+  };
+  // small launches (latency-bound: a few traces x a few thousand steps) skip the optional
+  // stagings — loading ~100 KB of tables per CTA costs more than the lookups it speeds up
+  const bool small = (double)a->n_traces * (double)a->n_steps < (double)(1 << 22);
+  auto search = [&](size_t lut_b) {
+    Cand b;
+    const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;
+    for (int staged = small ? 0 : 1; staged >= 0; --staged)
+      for (int threads : {1024, 512, 256, 128}) {
+        for (int wpg : {1, 2, 4, 8, 16}) {
+          const int wpc = threads / 32;
+          if (wpg > wpc) continue;
+          const int gpc = wpc / wpg;
+          if (wpg > 1 && gpc > 15) continue;  // named barriers 1..15
+          size_t o1, o2, o3;
+          const size_t smem = fixed0 + (staged ? seg_smem : 0) + (size_t)gpc * group_bytes(wpg, &o1, &o2, &o3);
+          if (smem > (size_t)smem_optin) continue;
+          const int per_sm = blocks_per_sm(fn, dev, threads, smem);
+          if (per_sm < 1) continue;
+          const int warps = per_sm * wpc;
+          if (warps > b.warps || (warps == b.warps && wpg < b.wpg && staged == (int)b.staged)) {
+            b.warps = warps, b.threads = threads, b.wpg = wpg, b.per_sm = per_sm, b.smem = smem;
+            b.staged = staged != 0;
+          }
+        }
       }
-      if (per_sm < 1) continue;
-      const int warps = per_sm * wpc;
-      if (warps > best_warps || (warps == best_warps && wpg < b_wpg)) {
-        best_warps = warps, b_threads = threads, b_wpg = wpg, b_per_sm = per_sm, b_smem = smem;
-      }
-    }
+    return b;
+  };
+  Cand c = search(lut_bytes);
+  bool big = false;
+  if (f32 && view.n_lut_big > 0 && !small) {
+    const Cand cb = search(a16((size_t)view.n_lut_big * 4));
+    if (cb.warps >= c.warps && cb.warps > 0 && (cb.staged || !c.staged)) c = cb, big = true;
   }
+  const size_t lut_b = big ? a16((size_t)view.n_lut_big * 4) : lut_bytes;  // the LUT staged
+  const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;
+  int best_warps = c.warps, b_threads = c.threads, b_wpg = c.wpg, b_per_sm = c.per_sm;
+  size_t b_smem = c.smem;
+  bool b_staged = c.staged;
   if (best_warps < 0)
     return "tables too large for shared memory (" + std::to_string(U) + " union bins, " +
            std::to_string(t.lut.size()) + " LUT entries)";
@@ -828,7 +951,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   pl.seg_len = seg_len;
   pl.ctas = (int)std::max<int64_t>(
       1, std::min<int64_t>((int64_t)nsm * b_per_sm, (a->n_traces * nseg + pl.gpc - 1) / pl.gpc));
-  pl.ws_prep = a16((size_t)(t.seg.size() / 4) * 64);
+  pl.ws_prep = seg_ws;
   pl.ws_split = nseg > 1 ? (size_t)a->n_traces *
                                ((size_t)U4 + (pen ? (size_t)nsegs : 0) + (size_t)M * 3) * sizeof(uint32_t)
                          : 0;
@@ -836,6 +959,9 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   EvalParams& P = pl.P;
   P = EvalParams{};
   P.tb = view;
+  P.lv = big ? view.lv_big : view.lv;
+  P.n_lut = big ? view.n_lut_big : view.n_lut;
+  P.n_level1 = big ? view.n_level1_big : view.n_level1;
   P.caps = a->caps;
   P.T = a->n_traces;
   P.S = a->n_steps;
@@ -857,10 +983,12 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.hstride = hs;
   P.U4 = U4;
   P.NSEG = nsegs;
-  P.off_vio = (int32_t)lut_bytes;
-  P.off_sig = (int32_t)(lut_bytes + vio_bytes);
-  P.off_ghist = (int32_t)(lut_bytes + vio_bytes + sig_bytes);
-  P.off_groups = (int32_t)fixed;
+  P.off_vio = (int32_t)lut_b;
+  P.off_sig = (int32_t)(lut_b + vio_bytes);
+  P.off_ghist = (int32_t)(lut_b + vio_bytes + sig_bytes);
+  P.off_seg = (int32_t)fixed0;
+  P.seg_smem_bytes = b_staged ? (int32_t)seg_smem : 0;
+  P.off_groups = (int32_t)(fixed0 + (b_staged ? seg_smem : 0));
   size_t o1, o2, o3;
   P.group_bytes = (int32_t)group_bytes(pl.wpg, &o1, &o2, &o3);
   P.off_g_sw = (int32_t)o1;
@@ -893,13 +1021,19 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   if (a->workspace == nullptr || a->workspace_bytes < need)
     return "workspace too small: need " + std::to_string(need) + " bytes (cs_eval_workspace_size)";
   unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace);
-  double2* segrec = reinterpret_cast<double2*>(ws);
-  P.segrec = segrec;
+  {
+    const int NS = P.NSEG, M = t.M;
+    P.seg_hdr = reinterpret_cast<const uint32_t*>(ws);
+    P.seg_idle = reinterpret_cast<const int32_t*>(ws + (size_t)((NS + 3) & ~3) * 4);
+    P.seg_val = reinterpret_cast<const double*>(ws + (size_t)((NS + 3) & ~3) * 4 + (size_t)((M * 3 + 3) & ~3) * 4);
+  }
   // bits of the exact hi part: counts up to S must keep sum(count x hi) below 2^53 quanta
   int L = 52;
   while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
   int launches = 0;
-  prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, segrec);
+  prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, P.NSEG,
+                                                    const_cast<uint32_t*>(P.seg_hdr), const_cast<int32_t*>(P.seg_idle),
+                                                    const_cast<double*>(P.seg_val));
   CS_CUDA_TRY(cudaGetLastError());
   ++launches;
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));

@@ -18,6 +18,7 @@
 // maps union bin -> grid bin through umap.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <map>
@@ -131,6 +132,60 @@ struct LutBuilder {
     return (id << 16) | kRedirect | ns;
   }
 };
+
+// Level-1 shift search + build for one LUT size (budgets in 32-bit entries).
+std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32, uint32_t level1_max,
+                      uint32_t total_budget, Tables::Lut& out) {
+  // fp32: level-1 buckets k = (bits >> S1) - KBASE with an empty guard bucket below the first
+  // threshold and one above the last (the kernel clamps k, not the cap). fp64: clamp the cap.
+  const uint32_t width = f32 ? 32 : 64;
+  auto range = [&](uint32_t s, uint64_t* kb, uint64_t* nb) -> bool {
+    if (f32) {
+      // s >= 1 keeps ((int32)bits >> s) - KBASE free of int32 overflow for sign-bit patterns
+      if (s == 0 || (T.front() >> s) == 0) return false;  // and leaves room for the guard bucket
+      *kb = (T.front() >> s) - 1;
+      *nb = (T.back() >> s) - *kb + 2;
+    } else {
+      *kb = (uint64_t)t.lo >> s;
+      *nb = ((uint64_t)t.hi >> s) - *kb + 1;
+    }
+    return true;
+  };
+  uint32_t best_s = width - 2;
+  size_t best_total = ~(size_t)0;
+  for (uint32_t s = 0; s + 1 < width; ++s) {
+    if (f32 && s > 30) break;
+    uint64_t kb, nb;
+    if (!range(s, &kb, &nb) || nb > level1_max) continue;
+    LutBuilder lbld(T, f32);
+    for (uint64_t k = 0; k < nb; ++k) lbld.make((kb + k) << s, s);
+    const size_t total = nb + lbld.sub.size();
+    if (total < best_total && !(f32 && lbld.n_sub > kMaxSub32)) {
+      best_total = total;
+      best_s = s;
+    }
+    if (total <= total_budget && !(f32 && lbld.n_sub > kMaxSub32)) {
+      best_s = s;
+      break;
+    }
+  }
+  const uint32_t s = best_s;
+  uint64_t kb, nb;
+  if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
+  LutBuilder lbld(T, f32, f32 ? &t.vio : nullptr);
+  out.kbase = kb;
+  std::vector<uint32_t> level1(nb);
+  for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
+  if (f32 && lbld.n_sub > kMaxSub32) return "threshold LUT needs more than 2048 sub-tables";
+  if (lbld.n_sub > 65535) return "threshold LUT needs more than 65535 sub-tables";
+  out.shift1 = s;
+  out.n_level1 = (uint32_t)nb;
+  out.n_sub = lbld.n_sub;
+  out.n_unsafe = lbld.unsafe;
+  out.lut = std::move(level1);
+  out.lut.insert(out.lut.end(), lbld.sub.begin(), lbld.sub.end());
+  return std::string();
+}
 
 }  // namespace
 
@@ -325,61 +380,27 @@ std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap
   }
 
   // ---- LUT over the union thresholds ----
-  // fp32: level-1 buckets k = (bits >> S1) - KBASE with an empty guard bucket below the first
-  // threshold and one above the last (the kernel clamps k, not the cap). fp64: clamp the cap.
+  // Two sizes: the default LUT (every kernel) and, when a finer level 1 exists, a big one that
+  // eval_kernel takes whenever it fits in shared memory without costing resident warps (fewer
+  // multi-threshold buckets -> fewer warps on the redirect path).
   const std::vector<uint64_t>& T = t.thresholds;
   t.lo = (int64_t)T.front() - 1;
   t.hi = (int64_t)T.back();
-  const uint32_t width = f32 ? 32 : 64;
-  const uint32_t kLevel1Max = 8192, kTotalBudget = 12288;
-  auto range = [&](uint32_t s, uint64_t* kb, uint64_t* nb) -> bool {
-    if (f32) {
-      // s >= 1 keeps ((int32)bits >> s) - KBASE free of int32 overflow for sign-bit patterns
-      if (s == 0 || (T.front() >> s) == 0) return false;  // and leaves room for the guard bucket
-      *kb = (T.front() >> s) - 1;
-      *nb = (T.back() >> s) - *kb + 2;
-    } else {
-      *kb = (uint64_t)t.lo >> s;
-      *nb = ((uint64_t)t.hi >> s) - *kb + 1;
-    }
-    return true;
-  };
-  uint32_t best_s = width - 2;
-  size_t best_total = ~(size_t)0;
-  for (uint32_t s = 0; s + 1 < width; ++s) {
-    if (f32 && s > 30) break;
-    uint64_t kb, nb;
-    if (!range(s, &kb, &nb) || nb > kLevel1Max) continue;
-    LutBuilder lbld(T, f32);
-    for (uint64_t k = 0; k < nb; ++k) lbld.make((kb + k) << s, s);
-    const size_t total = nb + lbld.sub.size();
-    if (total < best_total && !(f32 && lbld.n_sub > kMaxSub32)) {
-      best_total = total;
-      best_s = s;
-    }
-    if (total <= kTotalBudget && !(f32 && lbld.n_sub > kMaxSub32)) {
-      best_s = s;
-      break;
-    }
+  uint32_t l1max = 8192;
+  if (const char* e = std::getenv("CS_LUT_LEVEL1_MAX")) l1max = (uint32_t)std::atoi(e);  // tuning only
+  std::string err = build_lut(t, T, f32, l1max, l1max + l1max / 2, t.lut_main);
+  if (!err.empty()) return err;
+  if (f32) {
+    err = build_lut(t, T, f32, 20480, 24576, t.lut_big);
+    if (!err.empty() || t.lut_big.shift1 >= t.lut_main.shift1) t.lut_big = Tables::Lut{};
   }
-  {
-    const uint32_t s = best_s;
-    uint64_t kb, nb;
-    if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
-    LutBuilder lbld(T, f32, f32 ? &t.vio : nullptr);
-    t.kbase = kb;
-    std::vector<uint32_t> level1(nb);
-    for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
-    if (f32 && lbld.n_sub > kMaxSub32) return "threshold LUT needs more than 2048 sub-tables";
-    if (lbld.n_sub > 65535) return "threshold LUT needs more than 65535 sub-tables";
-    if (f32 && t.U > 65535) return "more than 65534 distinct power thresholds across grids";
-    t.shift1 = s;
-    t.n_level1 = (uint32_t)nb;
-    t.n_sub = lbld.n_sub;
-    t.n_unsafe = lbld.unsafe;
-    t.lut = std::move(level1);
-    t.lut.insert(t.lut.end(), lbld.sub.begin(), lbld.sub.end());
-  }
+  if (f32 && t.U > 65535) return "more than 65534 distinct power thresholds across grids";
+  t.kbase = t.lut_main.kbase;
+  t.shift1 = t.lut_main.shift1;
+  t.n_level1 = t.lut_main.n_level1;
+  t.n_sub = t.lut_main.n_sub;
+  t.n_unsafe = t.lut_main.n_unsafe;
+  t.lut = t.lut_main.lut;
   return std::string();
 }
 

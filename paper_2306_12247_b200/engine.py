@@ -136,12 +136,14 @@ class Tables:
             self._bins[m] = gb
         return gb
 
-    def lookup_host(self, caps: np.ndarray) -> np.ndarray:
-        """Host restatement of the device LUT search (test hook, not used by the product path)."""
+    def lookup_host(self, caps: np.ndarray, lut: str = "main") -> np.ndarray:
+        """Host restatement of the device LUT search (test hook, not used by the product path).
+        ``lut="big"`` searches the finer fp32 LUT the evaluation kernel stages when it fits."""
         dt = np.float32 if self.cap_dtype == "f32" else np.float64
         caps = np.ascontiguousarray(caps, dtype=dt)
         out = np.zeros(caps.shape[0], dtype=np.int32)
-        N.check(N.lib().cs_tables_lookup_host(self._h, caps.ctypes.data, caps.shape[0], out.ctypes.data))
+        N.check(N.lib().cs_tables_lookup_host_lut(self._h, caps.ctypes.data, caps.shape[0],
+                                                  {"main": 0, "big": 1}[lut], out.ctypes.data))
         return out
 
     # ---- evaluation ----

@@ -51,12 +51,14 @@ def test_lut_and_decode_match_reference(dtype):
         t = Tables.stage([grid], dtype, batching_mtl=case["batching_mtl"], multi_tenant_bs=case["multi_tenant_bs"])
         idx = [i for i, c in enumerate(case["caps"]) if dtype == "f64" or is_f32(c)]
         caps = np.array([case["caps"][i] for i in idx])
-        ub = t.lookup_host(caps)
-        for p, regime in enumerate(REGIMES):
-            got = decode(grid, t, 0, ub, p)
-            want = [case["select"][regime][i] for i in idx]
-            assert got == want, (case["name"], dtype, regime)
-            checked += len(idx)
+        luts = ["main"] + (["big"] if t.info.lut_big_entries else [])
+        for lut in luts:
+            ub = t.lookup_host(caps, lut)
+            for p, regime in enumerate(REGIMES):
+                got = decode(grid, t, 0, ub, p)
+                want = [case["select"][regime][i] for i in idx]
+                assert got == want, (case["name"], dtype, regime, lut)
+                checked += len(idx)
     assert checked > 5000
 
 
@@ -94,6 +96,9 @@ def test_dense_fine_grid_lut_is_exact():
                                                               np.nextafter(pws, 0), np.nextafter(pws, 400)]))):
         t = Tables.stage([g], dtype)
         ub = t.lookup_host(caps)
+        if dtype == "f32":  # the finer LUT the kernel prefers must give the same bins
+            assert t.info.lut_big_entries > 0 and t.info.lut_big_shift < t.info.lut_shift
+            assert np.array_equal(t.lookup_host(caps, "big"), ub)
         gb = t.grid_bins(0)
         idx = oracle.Index(ga, "combination")
         for cap, u in zip(caps.astype(np.float64)[::7], ub[::7]):
@@ -116,7 +121,8 @@ def test_lut_leaves_proven_violation_free():
     for case in doc["cases"]:
         grid = grid_from_doc(case["grid"])
         t = Tables.stage([grid], "f32", batching_mtl=case["batching_mtl"], multi_tenant_bs=case["multi_tenant_bs"])
-        assert t.info.lut_unsafe_leaves == 0, case["name"]
+        assert t.info.lut_unsafe_leaves == 0 and t.info.lut_big_unsafe_leaves == 0, case["name"]
         assert t.info.n_segments >= 3
     g = synthesize_grid(SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
-    assert Tables.stage([g], "f32").info.lut_unsafe_leaves == 0
+    info = Tables.stage([g], "f32").info
+    assert info.lut_unsafe_leaves == 0 and info.lut_big_unsafe_leaves == 0
