@@ -77,6 +77,8 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, lib)
+    for o in objs:  # objects are scratch: keep the GPU snapshot small
+        Path(o).unlink(missing_ok=True)
     (LIBDIR / (lib.stem + ".ptxas.log")).write_text("\n".join(log))
     if verbose:
         print("\n".join(log))

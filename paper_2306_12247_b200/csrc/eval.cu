@@ -407,7 +407,10 @@ struct Lut32 {
     return lut[k];
   }
   __device__ __forceinline__ static uint32_t leaf(uint32_t e, uint32_t x, uint32_t mask) {
-    return (e + ((x & mask) << 2)) >> 16;  // carries into bit 16 iff the bucket's threshold <= cap
+    // (e + (low bits << 2)) carries into bit 16 iff the bucket's threshold <= cap; the high half
+    // is taken with PRMT so the histogram address becomes one LEA (bin * 4 + base) instead of the
+    // SHF + LOP3 + IADD the compiler otherwise folds (>> 16) * 4 into
+    return __byte_perm(e + ((x & mask) << 2), 0u, 0x4432);
   }
   // resolve through redirect sub-tables; ORs the final leaf's "unproven" bit into flags
   __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t x, uint32_t& flags) const {
@@ -542,7 +545,6 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
   // rolling software pipeline: each vector's reload is issued as soon as it is consumed, so a
   // warp keeps 3-4 128-bit loads per lane in flight while it works (not 4, then 0)
   int v = gtid;
-#ifndef CS_ROLLING
   for (; v + 3 * gsize < nvf; v += 4 * gsize) {
     const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
     const uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
@@ -553,28 +555,6 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     vec4(r2, v + 2 * gsize);
     vec4(r3, v + 3 * gsize);
   }
-#else
-  if (v + 3 * gsize < nvf) {
-    uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
-    uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
-    uint4 r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16);
-    uint4 r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
-    for (;;) {
-      const int vn = v + 4 * gsize;
-      const bool more = vn + 3 * gsize < nvf;
-      vec4(r0, v);
-      if (more) r0 = ldg_stream(vrow + (size_t)vn * 16);
-      vec4(r1, v + gsize);
-      if (more) r1 = ldg_stream(vrow + (size_t)(vn + gsize) * 16);
-      vec4(r2, v + 2 * gsize);
-      if (more) r2 = ldg_stream(vrow + (size_t)(vn + 2 * gsize) * 16);
-      vec4(r3, v + 3 * gsize);
-      if (more) r3 = ldg_stream(vrow + (size_t)(vn + 3 * gsize) * 16);
-      v = vn;
-      if (!more) break;
-    }
-  }
-#endif
   for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
   // tail (< 4 caps at the very end of a trace)
   for (int i = 4 * nvf + gtid; i < n; i += gsize) {
