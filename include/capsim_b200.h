@@ -207,6 +207,32 @@ int cs_select_sampling(const cs_tables* t, int32_t grid, const double* caps_dev,
 int cs_generate_traces(float* caps_dev, int64_t n_traces, int64_t n_steps, int64_t ld, int64_t first_trace_id,
                        int32_t step_seconds, int32_t kind, float peak_w, uint64_t seed, void* stream);
 
+/* ---- trace ingestion fast path (load_trace, trace.py:87-169) ----
+ * CSV text -> fp64 samples on the host with the reference's rules (header, blank rows, 2
+ * fields, ISO-8601 UTC timestamps on the step grid, finite non-negative capacities, whole-step
+ * gaps forward-filled only with gap_fill). The native grammar is narrow (ASCII; timestamps
+ * YYYY-MM-DD(T| )HH:MM:SS[.f{1,6}][Z|z|+00:00|-00:00]; plain decimal capacities): a file inside
+ * it parses to exactly the reference's samples (status CS_OK); anything else, including every
+ * error, reports CS_E_UNSUPPORTED in its info and the caller applies the reference rules
+ * itself (paper_2306_12247_b200/trace.py) to produce the identical outcome or exception. */
+typedef struct cs_traces cs_traces; /* parsed traces (host memory, library-owned) */
+typedef struct {
+  int64_t n_values;      /* samples after forward-fill (len(PowerTrace.values)) */
+  int64_t start_unix_us; /* first row's UTC timestamp (PowerTrace.start_time), us since 1970-01-01 */
+  int32_t status;        /* CS_OK or CS_E_UNSUPPORTED (see above) */
+  int32_t line;          /* 1-based line where the native parser stopped (status != CS_OK) */
+} cs_trace_info;
+/* n files, parsed on n_threads host threads (<= 0: all hardware threads). */
+int cs_traces_parse_files(const char* const* paths, int32_t n, int64_t step_seconds, int32_t gap_fill,
+                          int32_t n_threads, cs_traces** out);
+int cs_traces_parse_text(const char* text, int64_t len, int64_t step_seconds, int32_t gap_fill, cs_traces** out);
+int cs_traces_info(const cs_traces* t, int32_t i, cs_trace_info* info);
+int cs_traces_copy(const cs_traces* t, int32_t i, double* out); /* n_values doubles */
+/* All traces (each CS_OK with n_steps samples) into a row-major [n][ld] host matrix of CS_CAP_F32
+ * (round to nearest) or CS_CAP_F64; columns n_steps..ld-1 are zeroed. */
+int cs_traces_pack(const cs_traces* t, int32_t dtype, int64_t n_steps, int64_t ld, void* out, int32_t n_threads);
+void cs_traces_destroy(cs_traces* t);
+
 #ifdef __cplusplus
 }
 #endif

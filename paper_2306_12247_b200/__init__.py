@@ -76,11 +76,15 @@ from .sim import (
 )
 from .trace import (
     PowerTrace,
+    TraceMatrix,
     TraceStats,
     load_trace,
+    load_trace_matrix,
+    load_traces,
     normalize_display,
     normalize_trace,
     save_trace,
+    trace_array,
     trace_csv_text,
     trace_stats,
 )
@@ -97,8 +101,8 @@ __all__ = [
     "load_grid", "load_report", "load_trace", "normalize_display", "normalize_trace", "profiling_cost",
     "report_from_dict", "report_json_text", "report_to_dict", "sampling_policy", "sampling_steps", "save_grid", "save_report",
     "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
-    "slice_report", "synthesize_grid", "trace_csv_text", "trace_stats",
-    "Tables", "EvalResult", "HostEngine", "generate_traces",
+    "slice_report", "synthesize_grid", "trace_array", "trace_csv_text", "trace_stats",
+    "Tables", "EvalResult", "HostEngine", "generate_traces", "TraceMatrix", "load_traces", "load_trace_matrix",
     "REACTIVE", "ControlEvent", "ControllerReport", "ControllerState", "ControlMode", "EventKind",
     "event_log_csv_text", "moving_average_prediction", "proactive", "replay", "replay_many", "step_proactive",
     "step_reactive",

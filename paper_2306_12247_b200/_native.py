@@ -38,6 +38,8 @@ EXPORTS = (
     "cs_select_caps", "cs_feasible_caps",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
     "cs_replay", "cs_generate_traces", "cs_select_sampling",
+    "cs_traces_parse_files", "cs_traces_parse_text", "cs_traces_info", "cs_traces_copy", "cs_traces_pack",
+    "cs_traces_destroy",
 )
 
 
@@ -111,6 +113,10 @@ class EvalArgs(C.Structure):
     ]
 
 
+class TraceInfo(C.Structure):
+    _fields_ = [("n_values", C.c_int64), ("start_unix_us", C.c_int64), ("status", C.c_int32), ("line", C.c_int32)]
+
+
 class ReplayStep(C.Structure):
     _fields_ = [("measured_power_w", C.c_double), ("bin_reactive", C.c_uint16), ("bin_final", C.c_uint16),
                 ("kind_bits", C.c_uint8), ("pad", C.c_uint8 * 3)]
@@ -152,6 +158,12 @@ def _declare(L: C.CDLL) -> None:
         "cs_generate_traces": ([vp, i64, i64, i64, i64, i32, i32, C.c_float, C.c_uint64, vp], C.c_int),
         "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),
         "cs_select_sampling": ([vp, i32, vp, i64, i64, i64, i64, i64, C.c_uint64, i64, vp, vp, vp], C.c_int),
+        "cs_traces_parse_files": ([P(C.c_char_p), i32, i64, i32, i32, P(vp)], C.c_int),
+        "cs_traces_parse_text": ([C.c_char_p, i64, i64, i32, P(vp)], C.c_int),
+        "cs_traces_info": ([vp, i32, P(TraceInfo)], C.c_int),
+        "cs_traces_copy": ([vp, i32, vp], C.c_int),
+        "cs_traces_pack": ([vp, i32, i64, i64, vp, i32], C.c_int),
+        "cs_traces_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -13,7 +13,7 @@ from conftest import ROOT
 
 def header_symbols() -> set[str]:
     text = (ROOT / "include" / "capsim_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:const\s+char\s*\*|int)\s+(cs_\w+)\s*\(", text, flags=re.M))
+    return set(re.findall(r"^\s*(?:const\s+char\s*\*|int|void)\s+(cs_\w+)\s*\(", text, flags=re.M))
 
 
 def test_header_and_binding_agree():
