@@ -26,6 +26,16 @@ from .controller import (
     step_proactive,
     step_reactive,
 )
+from .columnar import (
+    ColumnarRun,
+    eval_table,
+    histogram_table,
+    load_columnar,
+    reports_table,
+    save_columnar,
+    steps_table,
+    table_to_reports,
+)
 from .engine import EvalResult, HostEngine, Tables, generate_traces
 from .errors import CapsimError, ParseError, ValidationError
 from .policy import (
@@ -103,6 +113,8 @@ __all__ = [
     "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
     "slice_report", "synthesize_grid", "trace_array", "trace_csv_text", "trace_stats",
     "Tables", "EvalResult", "HostEngine", "generate_traces", "TraceMatrix", "load_traces", "load_trace_matrix",
+    "ColumnarRun", "eval_table", "histogram_table", "load_columnar", "reports_table", "save_columnar", "steps_table",
+    "table_to_reports",
     "REACTIVE", "ControlEvent", "ControllerReport", "ControllerState", "ControlMode", "EventKind",
     "event_log_csv_text", "moving_average_prediction", "proactive", "replay", "replay_many", "step_proactive",
     "step_reactive",
