@@ -45,6 +45,7 @@ extern "C" {
 /* cs_eval flags */
 #define CS_FLAG_CHECK_VIOLATIONS 1u /* per-step power <= cap self-check (StepRecord, sim.py:50-54) */
 #define CS_FLAG_ACCUMULATE_HIST 2u  /* add into hist_out instead of overwriting it */
+#define CS_FLAG_SEGMENT_EPILOGUE 4u /* diagnostics: keep the segment epilogue where the per-bin one applies */
 
 /* One profiling grid (ProfileGrid, profile.py:57-106): n entries Config(mtl, bs) -> (ips, W). */
 typedef struct {

@@ -26,6 +26,7 @@ CS_CAP_F64 = 1
 
 CS_FLAG_CHECK_VIOLATIONS = 1
 CS_FLAG_ACCUMULATE_HIST = 2
+CS_FLAG_SEGMENT_EPILOGUE = 4
 
 TRACE_KINDS = {"solar": 0, "wind": 1, "mixed": 2, "iid": 3}
 

@@ -97,6 +97,12 @@ struct EvalParams {
   const int32_t* seg_idle;
   const double* seg_val;
   int32_t off_seg, seg_smem_bytes;
+  // bin epilogue (one grid, no penalty): per union bin u and policy p the {hi, lo} pairs of the
+  // step's throughput and energy, bin_val[(2p + j) * U4 + u] (j = 0 thr, 1 energy), staged at
+  // off_seg; bins u < fidle[p] are idle for policy p
+  const double2* bin_val;
+  int32_t bin_epi;
+  int32_t fidle[3];
   int32_t U4;    // histogram row stride (U rounded up to a multiple of 4)
   int32_t NSEG;  // selection segments over all grids x policies
   double omp;
@@ -130,7 +136,7 @@ __device__ __forceinline__ double2 split2(double v, int eq) {
 }
 
 __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, int nseg, uint32_t* hdr,
-                            int32_t* idlef, double* val) {  // L: see split2
+                            int32_t* idlef, double* val, double2* binval, int U4) {  // L: see split2
   __shared__ double red[2][256];
   const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
   const size_t ob = (size_t)mp * B;
@@ -156,6 +162,15 @@ __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, 
   frexp(red[1][0] > 0.0 ? red[1][0] : 1.0, &ee);
   et -= L;
   ee -= L;
+  if (binval) {  // bin epilogue tables (M == 1: union bins are the grid's bins)
+    const int p = mp % 3;
+    for (int r = threadIdx.x; r < B; r += blockDim.x) {
+      const bool idle = tb.sel[ob + r] < 0;
+      binval[(size_t)(2 * p) * U4 + r] = split2(idle ? 0.0 : tb.sthr[ob + r], et);
+      binval[(size_t)(2 * p + 1) * U4 + r] =
+          split2(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[ob + r], step), 3600.0), ee);
+    }
+  }
   const int k0 = tb.seg_off[mp], k1 = tb.seg_off[mp + 1];
   if (threadIdx.x == 0) idlef[mp] = (k1 > k0 && tb.sel[ob + tb.seg[k0].z] < 0) ? 1 : 0;
   for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
@@ -239,6 +254,63 @@ __device__ __forceinline__ double xreduce4(const double (&v)[4], int lane) {
   return __dadd_rn(c, __shfl_xor_sync(FULL, c, 1));
 }
 
+// Combine a group's per-warp sums (wpg > 1) and write grid m's three cs_agg records of trace t:
+// lane kLaneOf4[c] of warp 0 holds component c (thr hi, lo, energy hi, lo) of mine[p];
+// ired = idle steps (3) and switched steps (3).
+__device__ __forceinline__ void store_aggs(const EvalParams& P, int64_t t, int m, double (&mine)[3],
+                                           uint32_t (&ired)[6], const uint32_t* vcnt, double* scratch, int lane,
+                                           int wig, int nw, int gid_local, int gsize) {
+  const int M = P.tb.M;
+  if (nw > 1) {  // combine the warps of the group through shared scratch (18 + 6 words / warp)
+    double* d = scratch + wig * 24;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (lane == kLaneOf4[c]) d[4 * p + c] = mine[p];
+    if (lane == 0)
+      for (int j = 0; j < 6; ++j) d[12 + j] = __longlong_as_double((long long)ired[j]);
+    group_sync(gid_local, gsize);
+    if (wig == 0) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (lane == kLaneOf4[c])
+            for (int w = 1; w < nw; ++w) mine[p] = __dadd_rn(mine[p], scratch[w * 24 + 4 * p + c]);
+      for (int w = 1; w < nw; ++w)
+        for (int j = 0; j < 6; ++j) ired[j] += (uint32_t)__double_as_longlong(scratch[w * 24 + 12 + j]);
+    }
+    group_sync(gid_local, gsize);
+  }
+  if (wig == 0) {
+    // lane q (< 3) gathers policy q's six sums and writes its aggregate
+    double part[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double x0 = __shfl_sync(0xffffffffu, mine[0], kLaneOf4[c]);
+      const double x1 = __shfl_sync(0xffffffffu, mine[1], kLaneOf4[c]);
+      const double x2 = __shfl_sync(0xffffffffu, mine[2], kLaneOf4[c]);
+      part[c] = lane == 0 ? x0 : (lane == 1 ? x1 : x2);
+    }
+    if (lane < 3 && P.agg) {
+      dd tsum{part[0], 0.0}, esum{part[2], 0.0};
+      dd_add2(tsum, part[1], 0.0);
+      dd_add2(esum, part[3], 0.0);
+      const uint32_t id = lane == 0 ? ired[0] : (lane == 1 ? ired[1] : ired[2]);
+      const uint32_t sc = lane == 0 ? ired[3] : (lane == 1 ? ired[4] : ired[5]);
+      cs_agg a;
+      a.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
+      a.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
+      a.idle_steps = id;
+      a.switches = sc;
+      a.violations = vcnt ? vcnt[3 * m + lane] : 0;
+      a.num_steps = P.S;
+      P.agg[t * M * 3 + 3 * m + lane] = a;
+    }
+  }
+}
+
 // Per-trace epilogue: every (grid, policy) aggregate of _aggregate (sim.py:104-127) from the
 // group's prefix-summed histogram. Union bins with the same selected config form a segment
 // (staged in tb.seg); a segment's step count is C[hi] - C[lo-1]. Threads stride over a
@@ -297,55 +369,49 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
       ired[p] = __reduce_add_sync(0xffffffffu, idle);
       ired[3 + p] = PEN ? __reduce_add_sync(0xffffffffu, swc) : 0u;
     }
-    if (nw > 1) {  // combine the warps of the group through shared scratch (18 + 6 words / warp)
-      double* d = scratch + wig * 24;
+    store_aggs(P, t, m, mine, ired, vcnt, scratch, lane, wig, nw, gid_local, gsize);
+  }
+}
+
+// Bin epilogue (one grid, no switch penalty): every bin carries its three policies' values, so
+// the trace's sums are sum_u h[u] x v_p(u) straight from the histogram — no prefix scan, no
+// segment ranges — and the same pass folds h into the CTA histogram and re-zeroes it.
+template <typename GH>
+__device__ __forceinline__ void finish_trace_bins(const EvalParams& P, int64_t t, uint32_t* h, const uint32_t* vcnt,
+                                                  GH* ghist, const double2* bv, double* scratch, int gtid, int gsize,
+                                                  int gid_local) {
+  const int U = P.tb.U, U4 = P.U4;
+  const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
+  double a[3][4];
+  uint32_t idl[3] = {0u, 0u, 0u};
 #pragma unroll
-      for (int p = 0; p < 3; ++p)
+  for (int p = 0; p < 3; ++p) a[p][0] = a[p][1] = a[p][2] = a[p][3] = 0.0;
+  for (int u = gtid; u < U; u += gsize) {
+    const uint32_t c = h[u];
+    if (c == 0) continue;
+    h[u] = 0u;
+    if (ghist) atomicAdd(&ghist[u], (GH)c);
+    const double dc = (double)c;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (lane == kLaneOf4[c]) d[4 * p + c] = mine[p];
-      if (lane == 0)
-        for (int j = 0; j < 6; ++j) d[12 + j] = __longlong_as_double((long long)ired[j]);
-      group_sync(gid_local, gsize);
-      if (wig == 0) {
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (lane == kLaneOf4[c])
-              for (int w = 1; w < nw; ++w) mine[p] = __dadd_rn(mine[p], scratch[w * 24 + 4 * p + c]);
-        for (int w = 1; w < nw; ++w)
-          for (int j = 0; j < 6; ++j) ired[j] += (uint32_t)__double_as_longlong(scratch[w * 24 + 12 + j]);
-      }
-      group_sync(gid_local, gsize);
-    }
-    if (wig == 0) {
-      // lane q (< 3) gathers policy q's six sums and writes its aggregate
-      double part[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double x0 = __shfl_sync(0xffffffffu, mine[0], kLaneOf4[c]);
-        const double x1 = __shfl_sync(0xffffffffu, mine[1], kLaneOf4[c]);
-        const double x2 = __shfl_sync(0xffffffffu, mine[2], kLaneOf4[c]);
-        part[c] = lane == 0 ? x0 : (lane == 1 ? x1 : x2);
-      }
-      if (lane < 3 && P.agg) {
-        dd tsum{part[0], 0.0}, esum{part[2], 0.0};
-        dd_add2(tsum, part[1], 0.0);
-        dd_add2(esum, part[3], 0.0);
-        const uint32_t id = lane == 0 ? ired[0] : (lane == 1 ? ired[1] : ired[2]);
-        const uint32_t sc = lane == 0 ? ired[3] : (lane == 1 ? ired[4] : ired[5]);
-        cs_agg a;
-        a.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
-        a.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
-        a.idle_steps = id;
-        a.switches = sc;
-        a.violations = vcnt ? vcnt[3 * m + lane] : 0;
-        a.num_steps = P.S;
-        P.agg[t * M * 3 + 3 * m + lane] = a;
-      }
+    for (int p = 0; p < 3; ++p) {
+      const double2 vt = bv[(size_t)(2 * p) * U4 + u];
+      const double2 ve = bv[(size_t)(2 * p + 1) * U4 + u];
+      a[p][0] = __fma_rn(dc, vt.x, a[p][0]);
+      a[p][1] = __fma_rn(dc, vt.y, a[p][1]);
+      a[p][2] = __fma_rn(dc, ve.x, a[p][2]);
+      a[p][3] = __fma_rn(dc, ve.y, a[p][3]);
+      idl[p] += u < P.fidle[p] ? c : 0u;
     }
   }
+  double mine[3];
+  uint32_t ired[6];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    mine[p] = xreduce4(a[p], lane);
+    ired[p] = __reduce_add_sync(0xffffffffu, idl[p]);
+    ired[3 + p] = 0u;
+  }
+  store_aggs(P, t, 0, mine, ired, vcnt, scratch, lane, wig, nw, gid_local, gsize);
 }
 
 // Scan + epilogue over a group histogram (smem in the main kernel, global in finalize); the
@@ -652,7 +718,10 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   uint32_t* s_seghdr = reinterpret_cast<uint32_t*>(smem + P.off_seg);
   int32_t* s_segidle = reinterpret_cast<int32_t*>(s_seghdr + ((P.NSEG + 3) & ~3));
   double2* s_segval = reinterpret_cast<double2*>(s_segidle + ((M * 3 + 3) & ~3));
-  if (seg_staged) {
+  double2* s_binval = reinterpret_cast<double2*>(smem + P.off_seg);
+  if (!PEN && P.bin_epi) {
+    for (int i = threadIdx.x; i < 6 * P.U4; i += blockDim.x) s_binval[i] = __ldg(P.bin_val + i);
+  } else if (seg_staged) {
     const int NS = P.NSEG, NV = PEN ? 3 : 2;
     const double2* gv = reinterpret_cast<const double2*>(P.seg_val);
     for (int i = threadIdx.x; i < NS; i += blockDim.x) s_seghdr[i] = __ldg(P.seg_hdr + i);
@@ -718,7 +787,9 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
         }
       }
       uint32_t* gh = want_hist ? s_ghist : (uint32_t*)nullptr;
-      if (seg_staged)  // two instantiations so each reads its tables with a known address space
+      if (!PEN && P.bin_epi)
+        finish_trace_bins(P, t, h, vcnt, gh, s_binval, scratch, gtid, gsize, gid_local);
+      else if (seg_staged)  // two instantiations so each reads its tables with a known address space
         finish_trace<PEN>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
       else
         finish_trace<PEN>(P, t, h, sw, vcnt, gh, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val),
@@ -812,6 +883,7 @@ void* pick_kernel(bool f32, bool pen, bool step, bool vio) {
 }
 
 size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+size_t bin_bytes_of(const EvalParams& P) { return (size_t)6 * P.U4 * 16; }
 
 // Resident CTAs per SM for (kernel, block size, dynamic smem), memoised: the plan search asks
 // for dozens of candidates per launch and the occupancy API dominates small launches otherwise.
@@ -854,7 +926,11 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   // workspace; the kernel stages hdr, flags and the 4 (6 with a penalty) value arrays it reads
   const size_t seg_hdr_b = (size_t)((nsegs + 3) & ~3) * 4, seg_idle_b = (size_t)((M * 3 + 3) & ~3) * 4;
   const size_t seg_ws = a16(seg_hdr_b + seg_idle_b + (size_t)6 * nsegs * 8);
-  const size_t seg_smem = a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
+  // one grid without a penalty: the bin epilogue's per-bin tables replace the segment tables
+  const bool bin_epi = !pen && M == 1 && (double)a->n_traces * (double)a->n_steps >= (double)(1 << 22) &&
+                       !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
+  const size_t bin_bytes = (size_t)6 * U4 * 16;
+  const size_t seg_smem = bin_epi ? bin_bytes : a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
   const int hs = 1;
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
     size_t gb = a16((size_t)U4 * 4 * hs);
@@ -931,7 +1007,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   pl.seg_len = seg_len;
   pl.ctas = (int)std::max<int64_t>(
       1, std::min<int64_t>((int64_t)nsm * b_per_sm, (a->n_traces * nseg + pl.gpc - 1) / pl.gpc));
-  pl.ws_prep = seg_ws;
+  pl.ws_prep = seg_ws + (bin_epi && b_staged ? bin_bytes : 0);
   pl.ws_split = nseg > 1 ? (size_t)a->n_traces *
                                ((size_t)U4 + (pen ? (size_t)nsegs : 0) + (size_t)M * 3) * sizeof(uint32_t)
                          : 0;
@@ -968,6 +1044,12 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_ghist = (int32_t)(lut_b + vio_bytes + sig_bytes);
   P.off_seg = (int32_t)fixed0;
   P.seg_smem_bytes = b_staged ? (int32_t)seg_smem : 0;
+  P.bin_epi = (bin_epi && b_staged) ? 1 : 0;  // only with its tables in shared memory
+  for (int pp = 0; pp < 3; ++pp) {
+    int f = 0;
+    while (f < t.grid_bins[0] && t.sel[(size_t)pp * t.maxB + f] < 0) ++f;
+    P.fidle[pp] = f;
+  }
   P.off_groups = (int32_t)(fixed0 + (b_staged ? seg_smem : 0));
   size_t o1, o2, o3;
   P.group_bytes = (int32_t)group_bytes(pl.wpg, &o1, &o2, &o3);
@@ -1011,9 +1093,11 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   int L = 52;
   while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
   int launches = 0;
+  P.bin_val = P.bin_epi ? reinterpret_cast<const double2*>(ws + pl.ws_prep - bin_bytes_of(P)) : nullptr;
   prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, P.NSEG,
                                                     const_cast<uint32_t*>(P.seg_hdr), const_cast<int32_t*>(P.seg_idle),
-                                                    const_cast<double*>(P.seg_val));
+                                                    const_cast<double*>(P.seg_val), const_cast<double2*>(P.bin_val),
+                                                    P.U4);
   CS_CUDA_TRY(cudaGetLastError());
   ++launches;
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));

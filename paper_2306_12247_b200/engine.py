@@ -149,7 +149,7 @@ class Tables:
     # ---- evaluation ----
     def evaluate(self, caps, n_steps: int | None = None, *, step_seconds: int, switch_penalty_s: float = 0.0,
                  per_step: bool = False, check_violations: bool = True, want_hist: bool = True,
-                 accumulate_hist=None, stream=None) -> "EvalResult":
+                 accumulate_hist=None, stream=None, segment_epilogue: bool = False) -> "EvalResult":
         """N2+N3 over a device cap matrix ``caps`` [T, ld] (torch, cuda, dtype of the tables).
 
         Every (trace, grid, policy) aggregate of simulate() is produced in one pass; per-step
@@ -182,7 +182,8 @@ class Tables:
             a.step_seconds = int(step_seconds)
             a.switch_penalty_s = float(switch_penalty_s)
             a.flags = (N.CS_FLAG_CHECK_VIOLATIONS if check_violations else 0) | (
-                N.CS_FLAG_ACCUMULATE_HIST if accumulate_hist is not None else 0)
+                N.CS_FLAG_ACCUMULATE_HIST if accumulate_hist is not None else 0) | (
+                N.CS_FLAG_SEGMENT_EPILOGUE if segment_epilogue else 0)
             a.step_bins = bins.data_ptr() if bins is not None else None
             a.ld_bins = ld_bins
             a.agg = agg.data_ptr()

@@ -206,6 +206,28 @@ def test_engine_single_grid_vs_oracle(cs, torch, kind, pen):
     _engine_vs_oracle(cs, torch, [g], _random_caps(rng, 37, 1441, kind), 60, pen)
 
 
+def test_engine_bin_epilogue_vs_oracle_and_segments(cs, torch):
+    """>= 4M timesteps on one grid without a penalty take the per-bin epilogue (bench path, with
+    and without per-step output); it must match the oracle and the segment epilogue."""
+    rng = np.random.default_rng(21)
+    g = cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128, model_name="mobilenet-v1"))
+    caps = np.concatenate([_random_caps(rng, 300, 10080, "smooth"), _random_caps(rng, 120, 10080, "iid")])
+    res = _engine_vs_oracle(cs, torch, [g], caps, 60, 0.0)  # per-step variant
+    host = torch.from_numpy(np.ascontiguousarray(caps, np.float32)).cuda()
+    tables = cs.Tables.stage([g], "f32")
+    fast = tables.evaluate(host, 10080, step_seconds=60)
+    seg = tables.evaluate(host, 10080, step_seconds=60, segment_epilogue=True)
+    torch.cuda.synchronize()
+    for r in (fast, seg):
+        assert np.array_equal(r.idle_steps.cpu().numpy(), res.idle_steps.cpu().numpy())
+        assert np.array_equal(r.hist.cpu().numpy(), res.hist.cpu().numpy())
+        assert np.allclose(r.avg_throughput_ips.cpu().numpy(), res.avg_throughput_ips.cpu().numpy(), rtol=1e-12,
+                           atol=0)
+        assert np.allclose(r.energy_proxy_wh.cpu().numpy(), res.energy_proxy_wh.cpu().numpy(), rtol=1e-12, atol=0)
+    same = np.mean(fast.avg_throughput_ips.cpu().numpy() == seg.avg_throughput_ips.cpu().numpy())
+    assert same > 0.999
+
+
 def test_engine_multi_grid_vs_oracle(cs, torch):
     rng = np.random.default_rng(12)
     grids = [cs.synthesize_grid(cs.SynthParams(t_max_ips=float(rng.uniform(1000, 20000)), tau=float(rng.uniform(8, 128)),
