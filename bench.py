@@ -269,6 +269,7 @@ def main() -> None:
         N.check(N.lib().cs_eval_last_kernel_ms(C.byref(ms)))
         single.append(ms.value)
     kernel_ms = statistics.mean(single)
+    plan = tables.last_plan()
     elapsed_ms = max_over_ranks(elapsed_ms, dev)
     kernel_ms_max = max_over_ranks(kernel_ms, dev)
     ms_per_step = elapsed_ms / args.steps
@@ -314,7 +315,7 @@ def main() -> None:
                        "step_seconds": cfg["step_seconds"], "switch_penalty_s": cfg["penalty"],
                        "trace_kind": cfg["kind"], "parallelism": f"trace-sharded x{world}",
                        "l2": f"inputs {T_total * S * 4 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
-                       "policy_evaluations_per_step": T_total * S * M * 3},
+                       "policy_evaluations_per_step": T_total * S * M * 3, "plan": plan},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured"

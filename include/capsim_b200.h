@@ -142,6 +142,14 @@ int cs_eval(const cs_tables* t, const cs_eval_args* a, void* stream);
 int cs_eval_last_kernel_ms(float* ms);
 /* Number of kernels the last cs_eval launched. */
 int cs_eval_last_launches(int32_t* n);
+/* Launch plan of the last cs_eval on this thread (diagnostics / bench reporting). */
+typedef struct {
+  int32_t ctas, threads, warps_per_group, smem_bytes;
+  int32_t trace_segments; /* > 1: long traces split across worker groups (+ finalize kernel) */
+  int32_t lut_entries, lut_shift;
+  int32_t epilogue;       /* 0 segment tables from global, 1 staged segment tables, 2 per-bin */
+} cs_eval_plan;
+int cs_eval_last_plan(cs_eval_plan* out);
 
 /* ---- per-cap API: select_config (policy.py:172-188) and feasible_set (policy.py:151-169) as
  *      warp-per-query argmax (shuffle) / ballot kernels over the grid's raw entries ---- */

@@ -35,7 +35,7 @@ EXPORTS = (
     "cs_last_error", "cs_abi_version", "cs_device_query",
     "cs_tables_create", "cs_tables_destroy", "cs_tables_get_info", "cs_tables_grid_bins",
     "cs_tables_union_map", "cs_tables_lookup_host", "cs_tables_lookup_host_lut", "cs_tables_upload",
-    "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches",
+    "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches", "cs_eval_last_plan",
     "cs_select_caps", "cs_feasible_caps",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
     "cs_replay", "cs_generate_traces", "cs_select_sampling",
@@ -114,6 +114,11 @@ class EvalArgs(C.Structure):
     ]
 
 
+class EvalPlan(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("ctas", "threads", "warps_per_group", "smem_bytes", "trace_segments",
+                                         "lut_entries", "lut_shift", "epilogue")]
+
+
 class TraceInfo(C.Structure):
     _fields_ = [("n_values", C.c_int64), ("start_unix_us", C.c_int64), ("status", C.c_int32), ("line", C.c_int32)]
 
@@ -151,6 +156,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_eval": ([vp, P(EvalArgs), vp], C.c_int),
         "cs_eval_last_kernel_ms": ([P(C.c_float)], C.c_int),
         "cs_eval_last_launches": ([P(i32)], C.c_int),
+        "cs_eval_last_plan": ([P(EvalPlan)], C.c_int),
         "cs_select_caps": ([vp, i32, i32, vp, i64, vp, vp, vp], C.c_int),
         "cs_feasible_caps": ([vp, i32, i32, vp, i64, vp, vp], C.c_int),
         "cs_engine_create": ([i32, i64, i64, i32, P(vp)], C.c_int),

@@ -16,6 +16,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
 std::string eval_workspace(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, size_t* bytes);
 std::string last_kernel_ms(float* ms);
 int last_launches();
+cs_eval_plan last_plan();
 std::string launch_select(const DevTables& v, int g, int p, const double* caps, int64_t n, int32_t* sel, int64_t* cnt,
                           cudaStream_t st);
 std::string launch_feasible(const DevTables& v, int g, int p, const double* caps, int64_t n, uint32_t* mask,
@@ -348,6 +349,12 @@ int cs_eval_last_kernel_ms(float* ms) {
 int cs_eval_last_launches(int32_t* n) {
   if (!n) return fail(CS_E_INVALID, "null argument");
   *n = cs::last_launches();
+  return CS_OK;
+}
+
+int cs_eval_last_plan(cs_eval_plan* out) {
+  if (!out) return fail(CS_E_INVALID, "null argument");
+  *out = cs::last_plan();
   return CS_OK;
 }
 

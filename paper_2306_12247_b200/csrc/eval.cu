@@ -844,6 +844,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
 // ----------------------------------------------------------------------------------------
 thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
 thread_local int g_last_launches = 0;
+thread_local cs_eval_plan g_last_plan{};
 thread_local bool g_timed = false;
 
 struct Plan {
@@ -1126,6 +1127,14 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
     ++launches;
   }
   g_last_launches = launches;
+  g_last_plan.ctas = pl.ctas;
+  g_last_plan.threads = pl.threads;
+  g_last_plan.warps_per_group = pl.wpg;
+  g_last_plan.smem_bytes = (int32_t)pl.smem;
+  g_last_plan.trace_segments = pl.nseg;
+  g_last_plan.lut_entries = P.n_lut;
+  g_last_plan.lut_shift = (int32_t)P.lv.shift1;
+  g_last_plan.epilogue = P.bin_epi ? 2 : (P.seg_smem_bytes > 0 ? 1 : 0);
   return std::string();
 }
 
@@ -1136,5 +1145,6 @@ std::string last_kernel_ms(float* ms) {
 }
 
 int last_launches() { return g_last_launches; }
+cs_eval_plan last_plan() { return g_last_plan; }
 
 }  // namespace cs

@@ -198,6 +198,12 @@ class Tables:
             N.check(N.lib().cs_eval(self._h, C.byref(a), C.c_void_p(_stream_ptr(stream))))
         return EvalResult(self, agg, hist, bins, S, ws)
 
+    def last_plan(self) -> dict:
+        """Launch plan of the last evaluate() on this thread (CTAs, block size, group size, ...)."""
+        p = N.EvalPlan()
+        N.check(N.lib().cs_eval_last_plan(C.byref(p)))
+        return {f: getattr(p, f) for f, _ in p._fields_}
+
     def launch_count(self) -> int:
         n = C.c_int32()
         N.check(N.lib().cs_eval_last_launches(C.byref(n)))
