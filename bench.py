@@ -186,6 +186,7 @@ def main() -> None:
     ap.add_argument("--trace-kind", default=None, help="override: solar | wind | mixed | iid")
     ap.add_argument("--traces", type=int, default=None, help="override the total trace count")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time the host launch path instead of a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     args = ap.parse_args()
@@ -229,9 +230,18 @@ def main() -> None:
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 
+    # the step's launch sequence (prep, eval[, finalize]) is replayed from a CUDA graph: one graph
+    # launch per step instead of the Python/ctypes host path (which dominates C1/C2)
+    graph = None if args.no_graph else tables.capture(caps, S, step_seconds=cfg["step_seconds"],
+                                                        switch_penalty_s=cfg["penalty"], check_violations=True,
+                                                        want_hist=True)
+
     def step():
-        r = tables.evaluate(caps, S, step_seconds=cfg["step_seconds"], switch_penalty_s=cfg["penalty"],
-                            check_violations=True, want_hist=True)
+        if graph is not None:
+            r = graph.replay()
+        else:
+            r = tables.evaluate(caps, S, step_seconds=cfg["step_seconds"], switch_penalty_s=cfg["penalty"],
+                                check_violations=True, want_hist=True)
         reduce_histogram(r.hist)  # the single collective: global config histogram (int64, NCCL)
         return r
 
@@ -314,6 +324,7 @@ def main() -> None:
                        "grids": M, "policies": 3, "union_bins": tables.n_union_bins,
                        "step_seconds": cfg["step_seconds"], "switch_penalty_s": cfg["penalty"],
                        "trace_kind": cfg["kind"], "parallelism": f"trace-sharded x{world}",
+                       "launch": "cuda-graph replay" if graph is not None else "host path",
                        "l2": f"inputs {T_total * S * 4 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
                        "policy_evaluations_per_step": T_total * S * M * 3, "plan": plan},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",

@@ -102,6 +102,7 @@ struct EvalParams {
   // off_seg; bins u < fidle[p] are idle for policy p
   const double2* bin_val;
   int32_t bin_epi;
+  int32_t fin_split;  // finalize_kernel: per-grid CTAs on shared-memory histogram copies
   int32_t fidle[3];
   int32_t U4;    // histogram row stride (U rounded up to a multiple of 4)
   int32_t NSEG;  // selection segments over all grids x policies
@@ -321,11 +322,13 @@ __device__ __forceinline__ void store_aggs(const EvalParams& P, int64_t t, int m
 template <bool PEN>
 __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
                                          const uint32_t* vcnt, const uint32_t* shdr, const int32_t* sidle,
-                                         const double2* sval, double* scratch, int gtid, int gsize, int gid_local) {
+                                         const double2* sval, double* scratch, int gtid, int gsize, int gid_local,
+                                         int m_begin = 0, int m_end = -1) {
   const DevTables& tb = P.tb;
   const int M = tb.M, NS = P.NSEG;
   const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
-  for (int m = 0; m < M; ++m) {
+  if (m_end < 0) m_end = M;
+  for (int m = m_begin; m < m_end; ++m) {
     double mine[3];
     uint32_t ired[6];
 #pragma unroll
@@ -827,16 +830,33 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   }
 }
 
+// Epilogue of traces split across worker groups: one CTA per (trace, grid). Each CTA scans its
+// own shared-memory copy of the trace's partial histogram (the (t, 0) CTA also folds it into the
+// global histogram) and writes that grid's three aggregates — M-way parallel for the few long
+// traces of C1/C2-like sweeps instead of one CTA walking every grid's segments.
 template <bool PEN>
-__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EvalParams P) {
-  __shared__ double scratch[8 * 24];
+__global__ void __launch_bounds__(1024) finalize_kernel(const __grid_constant__ EvalParams P) {
+  extern __shared__ __align__(16) unsigned char fsmem[];
   const int64_t t = blockIdx.x;
   const int U4 = P.U4, M = P.tb.M;
-  uint32_t* h = P.part_hist + t * U4;
-  uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
+  // gridDim.y == M: per-grid CTAs on a shared-memory copy; gridDim.y == 1: one CTA per trace
+  // scanning the global partial histogram in place (unions too large for shared memory)
+  const bool split = P.fin_split != 0;
+  const int m = blockIdx.y;
+  uint32_t* hg = P.part_hist + t * U4;
+  uint32_t* h = split ? reinterpret_cast<uint32_t*>(fsmem) : hg;
+  double* scratch = reinterpret_cast<double*>(fsmem + (split ? (size_t)U4 * 4 : 0));
+  if (split)
+    for (int u = 4 * threadIdx.x; u < U4; u += 4 * blockDim.x)
+      *reinterpret_cast<uint4*>(h + u) = *reinterpret_cast<const uint4*>(hg + u);
+  __syncthreads();
+  group_scan(h, U4, m == 0 ? P.hist : (unsigned long long*)nullptr, reinterpret_cast<uint32_t*>(scratch),
+             threadIdx.x, blockDim.x, 0);
+  group_sync(0, blockDim.x);
+  const uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
   const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
-  finish_trace<PEN>(P, t, h, sw, vc, P.hist, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val),
-                    scratch, threadIdx.x, blockDim.x, 0);
+  epilogue<PEN>(P, t, h, sw, vc, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val), scratch,
+                threadIdx.x, blockDim.x, 0, split ? m : 0, split ? m + 1 : M);
 }
 
 // ----------------------------------------------------------------------------------------
@@ -953,14 +973,17 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   // small launches (latency-bound: a few traces x a few thousand steps) skip the optional
   // stagings — loading ~100 KB of tables per CTA costs more than the lookups it speeds up
   const bool small = (double)a->n_traces * (double)a->n_steps < (double)(1 << 22);
+  // tiny launches (fewer traces than SMs, <= 1M timesteps): a trace per CTA, all its warps on it
+  const bool tiny = a->n_traces < nsm && (double)a->n_traces * (double)a->n_steps <= (double)(1 << 20);
   auto search = [&](size_t lut_b) {
     Cand b;
     const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;
     for (int staged = small ? 0 : 1; staged >= 0; --staged)
       for (int threads : {1024, 512, 256, 128}) {
-        for (int wpg : {1, 2, 4, 8, 16}) {
+        for (int wpg : {1, 2, 4, 8, 16, 32}) {
           const int wpc = threads / 32;
           if (wpg > wpc) continue;
+          if (tiny ? wpg != wpc : wpg == 32) continue;  // tiny: one whole-CTA group per trace
           const int gpc = wpc / wpg;
           if (wpg > 1 && gpc > 15) continue;  // named barriers 1..15
           size_t o1, o2, o3;
@@ -968,7 +991,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
           if (smem > (size_t)smem_optin) continue;
           const int per_sm = blocks_per_sm(fn, dev, threads, smem);
           if (per_sm < 1) continue;
-          const int warps = per_sm * wpc;
+          const int warps = tiny ? wpc : per_sm * wpc;  // tiny: the biggest CTA, it runs alone
           if (warps > b.warps || (warps == b.warps && wpg < b.wpg && staged == (int)b.staged)) {
             b.warps = warps, b.threads = threads, b.wpg = wpg, b.per_sm = per_sm, b.smem = smem;
             b.staged = staged != 0;
@@ -1123,7 +1146,15 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   ++launches;
   if (pl.nseg > 1) {
     void* ff = pen ? (void*)finalize_kernel<true> : (void*)finalize_kernel<false>;
-    CS_CUDA_TRY(cudaLaunchKernel(ff, dim3((unsigned)a->n_traces), dim3(256), args, 0, st));
+    int optin = 232448;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t scr = 32 * 24 * 8;
+    const bool split = (size_t)P.U4 * 4 + scr <= (size_t)optin;
+    const size_t fsm = (split ? (size_t)P.U4 * 4 : 0) + scr;
+    P.fin_split = split ? 1 : 0;
+    CS_CUDA_TRY(cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    CS_CUDA_TRY(cudaLaunchKernel(ff, dim3((unsigned)a->n_traces, split ? (unsigned)t.M : 1u), dim3(1024), args, fsm,
+                                 st));
     ++launches;
   }
   g_last_launches = launches;

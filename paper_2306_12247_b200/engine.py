@@ -198,6 +198,10 @@ class Tables:
             N.check(N.lib().cs_eval(self._h, C.byref(a), C.c_void_p(_stream_ptr(stream))))
         return EvalResult(self, agg, hist, bins, S, ws)
 
+    def capture(self, caps, n_steps: int | None = None, **kw) -> EvalGraph:
+        """evaluate() as a replayable CUDA graph (same arguments; see EvalGraph)."""
+        return EvalGraph(self, caps, n_steps, **kw)
+
     def last_plan(self) -> dict:
         """Launch plan of the last evaluate() on this thread (CTAs, block size, group size, ...)."""
         p = N.EvalPlan()
@@ -278,6 +282,28 @@ class Tables:
                 row.append(d)
             out.append(row)
         return out
+
+
+class EvalGraph:
+    """One ``Tables.evaluate`` captured as a CUDA graph. ``replay()`` re-runs the launch sequence
+    (prep, eval, finalize kernels and the histogram memset) on the same device buffers in a single
+    graph launch: for latency-bound sweeps (a few traces) the host path — Python, ctypes, plan —
+    costs more than the kernels. Inputs are read from ``caps`` at replay time, so refill it in
+    place to evaluate new data; ``result`` holds the outputs of the latest replay."""
+
+    def __init__(self, tables: "Tables", caps, n_steps: int | None = None, **kw):
+        torch = _torch()
+        self.tables = tables
+        tables.evaluate(caps, n_steps, **kw)  # warm-up outside capture: upload, plan memo, events
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            self.result = tables.evaluate(caps, n_steps, **kw)
+        torch.cuda.synchronize()
+
+    def replay(self) -> "EvalResult":
+        self.graph.replay()
+        return self.result
 
 
 @dataclass
