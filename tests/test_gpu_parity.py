@@ -302,3 +302,23 @@ def test_engine_special_caps_match_host_lookup(cs, torch):
     top = t.n_union_bins - 1
     assert dev_bins[0] == 0 and dev_bins[1] == 0 and dev_bins[10] == top and dev_bins[11] == top
     assert int(res.violations.sum()) == 0
+
+
+@pytest.mark.parametrize("pen", [0.0, 30.0])
+def test_graph_replay_matches_evaluate(cs, torch, pen):
+    """Tables.capture: a CUDA-graph replay reads the caps buffer at replay time and reproduces
+    evaluate() exactly (tiny single-trace plan and split-trace finalize path)."""
+    rng = np.random.default_rng(31)
+    grids = [cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128, model_name="mobilenet-v1")),
+             cs.synthesize_grid(cs.SynthParams(mtl_cap=2, bs_cap=64, t_max_ips=4000.0, model_name="b"))]
+    for T, S in ((1, 1440), (2, 200_000)):
+        caps = torch.from_numpy(np.ascontiguousarray(_random_caps(rng, T, S, "smooth"), np.float32)).cuda()
+        tables = cs.Tables.stage(grids, "f32")
+        g = tables.capture(caps, S, step_seconds=60, switch_penalty_s=pen)
+        for _ in range(2):
+            r = g.replay()
+            torch.cuda.synchronize()
+            ref = tables.evaluate(caps, S, step_seconds=60, switch_penalty_s=pen)
+            torch.cuda.synchronize()
+            assert torch.equal(r.agg, ref.agg) and torch.equal(r.hist, ref.hist)
+            caps.mul_(0.75)  # new data in place: the next replay must see it
