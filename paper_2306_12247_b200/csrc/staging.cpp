@@ -151,8 +151,13 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
     }
     return true;
   };
+  // The finest level 1 whose LUT fits the budget; when none does (many grids: thousands of
+  // thresholds), the finest one within 12 % of the smallest LUT — a coarse level 1 of similar
+  // size sends nearly every cap through 2-3 sub-table levels (C3: shift 17 vs 12, 1.38x slower).
   uint32_t best_s = width - 2;
   size_t best_total = ~(size_t)0;
+  bool fits = false;
+  std::vector<std::pair<uint32_t, size_t>> cand;  // (shift, total) of the valid shifts
   for (uint32_t s = 0; s + 1 < width; ++s) {
     if (f32 && s > 30) break;
     uint64_t kb, nb;
@@ -160,15 +165,22 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
     LutBuilder lbld(T, f32);
     for (uint64_t k = 0; k < nb; ++k) lbld.make((kb + k) << s, s);
     const size_t total = nb + lbld.sub.size();
-    if (total < best_total && !(f32 && lbld.n_sub > kMaxSub32)) {
-      best_total = total;
+    if (f32 && lbld.n_sub > kMaxSub32) continue;
+    cand.emplace_back(s, total);
+    if (total < best_total) best_total = total, best_s = s;
+    if (total <= total_budget) {
       best_s = s;
-    }
-    if (total <= total_budget && !(f32 && lbld.n_sub > kMaxSub32)) {
-      best_s = s;
+      fits = true;
       break;
     }
   }
+  if (!fits)
+    for (const auto& c : cand)
+      if ((double)c.second <= 1.12 * (double)best_total) {
+        best_s = c.first;
+        break;
+      }
+  if (const char* e = std::getenv("CS_LUT_FORCE_SHIFT")) best_s = (uint32_t)std::atoi(e);  // tuning only
   const uint32_t s = best_s;
   uint64_t kb, nb;
   if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
