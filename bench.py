@@ -209,13 +209,20 @@ def main() -> None:
 
     import paper_2306_12247_b200 as cs
 
+    # one rank per GPU; CAPSIM_DIST_BACKEND=gloo lets several ranks share one device (a functional
+    # check of the sharded path on a single-GPU box; such timings are not bench numbers)
+    backend = os.environ.get("CAPSIM_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
     grids = make_grids(cfg["grids"])
     tables = cs.Tables.stage(grids, "f32")
@@ -325,6 +332,7 @@ def main() -> None:
                        "step_seconds": cfg["step_seconds"], "switch_penalty_s": cfg["penalty"],
                        "trace_kind": cfg["kind"], "parallelism": f"trace-sharded x{world}",
                        "launch": "cuda-graph replay" if graph is not None else "host path",
+                       "dist_backend": backend if world > 1 else None,
                        "l2": f"inputs {T_total * S * 4 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
                        "policy_evaluations_per_step": T_total * S * M * 3, "plan": plan},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
