@@ -199,6 +199,10 @@ def lib() -> C.CDLL:
     return _lib
 
 
+def last_error() -> str:
+    return lib().cs_last_error().decode("utf-8", "replace")
+
+
 def check(rc: int, invalid: type[Exception] = ValueError) -> None:
     """Map a C status to an exception. The Python layer validates arguments first with the
     reference's own messages (errors.py:4-22, policy.py:137-138, sim.py:147-150), so a C-side

@@ -118,10 +118,12 @@ def eval_table(result, *, trace_labels: Sequence[str], step_seconds: int, first_
 
 def histogram_table(tables, hist):
     """Global config histogram: steps per (grid, exhaustive policy, config); idle rows have null
-    mtl / bs. Integer-exact (Tables.config_histograms)."""
+    mtl / bs. Integer-exact (Tables.config_histograms). ``hist`` may also be the EvalResult
+    itself (required for grid-chunked runs, whose union-bin histograms are per chunk)."""
     pa = _pa()
     model, tag, mtl, bs, steps = [], [], [], [], []
-    for m, row in enumerate(tables.config_histograms(hist)):
+    rows = hist.config_histograms() if hasattr(hist, "config_histograms") else tables.config_histograms(hist)
+    for m, row in enumerate(rows):
         for p, d in enumerate(row):
             for cfg, c in sorted(d.items(), key=lambda kv: (kv[0] is not None, kv[0] or (0, 0))):
                 model.append(tables.grids[m].model_name)

@@ -30,7 +30,7 @@ namespace cs {
 //                                                    and caps above every threshold (and NaN)
 //                                                    in the top bin
 //   e  = lut[k]
-//   while e >= 0xFFFF0000 (redirect): s = e & 31; e = lut[SUB0 + ((e >> 5) & 0x7FF)*16 + ((bits >> s) & 15)]
+//   while e >= 0xFFF00000 (redirect): s = e & 31; e = lut[SUB0 + ((e >> 5) & 0x7FFF)*16 + ((bits >> s) & 15)]
 //   b  = (e + ((bits & mask(s)) << 2)) >> 16          mask(s) = (2^s - 1) & 0x3FFF
 // Leaf encoding: hi16 = base bin (thresholds below the bucket), lo16 = K where K = 0 when no
 // threshold lies in the bucket (or it sits on the bucket start: base is then +1), else
@@ -43,10 +43,10 @@ namespace cs {
 // leaf hi16 = base, lo16 = n in {0, 1}; b = base + (n && T64[base] <= u); redirect = 0x8000|s
 // with hi16 = sub-table index.
 // ---------------------------------------------------------------------------------------
-constexpr uint32_t kRedirect32 = 0xFFFF0000u;  // fp32 redirect marker (hi16 == 0xFFFF)
+constexpr uint32_t kRedirect32 = 0xFFF00000u;  // fp32 redirect marker (top 12 bits set; leaf bases < 0xFFF0)
 constexpr uint32_t kRedirect = 0x8000u;        // fp64 redirect flag
 constexpr int kSubFan = 16;
-constexpr uint32_t kMaxSub32 = 2048;
+constexpr uint32_t kMaxSub32 = 32768;  // 15-bit sub-table id in an fp32 redirect entry
 
 struct LutView {
   int64_t lo, hi;      // fp64: clamp bounds on the signed bit pattern
@@ -65,7 +65,7 @@ CS_HD uint32_t bin_f32(uint32_t bits, uint32_t s1, int32_t kbase, int32_t nb, ui
   uint32_t s = s1;
   while (e >= kRedirect32) {
     s = e & 31u;
-    e = lut[sub0 + ((e >> 5) & 0x7FFu) * kSubFan + ((bits >> s) & 15u)];
+    e = lut[sub0 + ((e >> 5) & 0x7FFFu) * kSubFan + ((bits >> s) & 15u)];
   }
   return (e + ((bits & ((1u << s) - 1u) & 0x3FFFu) << 2)) >> 16;
 }

@@ -486,7 +486,7 @@ struct Lut32 {
     uint32_t s = s1;
     while (e >= kRedirect32) {
       s = e & 31u;
-      e = lut[sub0 + ((e >> 5) & 0x7FFu) * kSubFan + ((x >> s) & 15u)];
+      e = lut[sub0 + ((e >> 5) & 0x7FFFu) * kSubFan + ((x >> s) & 15u)];
     }
     flags |= e;
     return leaf(e, x, ((1u << s) - 1u) & 0x3FFFu);
@@ -537,7 +537,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     }
     uint32_t b[4];
     const uint32_t any = e[0] | e[1] | e[2] | e[3];
-    if ((int32_t)any >= 0) {  // no redirect (marker 0xFFFF....; leaves have bit 31 clear while U < 2^15)
+    if ((int32_t)any >= 0) {  // no redirect (marker 0xFFF.....; leaves have bit 31 clear while U < 2^15)
       if (VIO) flags |= any;
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
@@ -549,7 +549,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
         sh[k] = L.s1;
         if (e[k] >= kRedirect32) {
           sh[k] = e[k] & 31u;
-          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
+          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
         }
       }
       if (e[0] >= kRedirect32 || e[1] >= kRedirect32 || e[2] >= kRedirect32 || e[3] >= kRedirect32) {
@@ -557,7 +557,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
         for (int k = 0; k < 4; ++k)
           while (e[k] >= kRedirect32) {
             sh[k] = e[k] & 31u;
-            e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
+            e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
           }
       }
       if (VIO) flags |= e[0] | e[1] | e[2] | e[3];

@@ -188,7 +188,7 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
   out.kbase = kb;
   std::vector<uint32_t> level1(nb);
   for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
-  if (f32 && lbld.n_sub > kMaxSub32) return "threshold LUT needs more than 2048 sub-tables";
+  if (f32 && lbld.n_sub > kMaxSub32) return "threshold LUT needs more than 32768 sub-tables";
   if (lbld.n_sub > 65535) return "threshold LUT needs more than 65535 sub-tables";
   out.shift1 = s;
   out.n_level1 = (uint32_t)nb;
@@ -406,7 +406,7 @@ std::string build_tables(const cs_grid_desc* grids, int32_t n_grids, int32_t cap
     err = build_lut(t, T, f32, 20480, 24576, t.lut_big);
     if (!err.empty() || t.lut_big.shift1 >= t.lut_main.shift1) t.lut_big = Tables::Lut{};
   }
-  if (f32 && t.U > 65535) return "more than 65534 distinct power thresholds across grids";
+  if (f32 && t.U > 0xFFF0) return "more than 65519 distinct power thresholds across grids";
   t.kbase = t.lut_main.kbase;
   t.shift1 = t.lut_main.shift1;
   t.n_level1 = t.lut_main.n_level1;

@@ -189,7 +189,15 @@ class Tables:
             a.agg = agg.data_ptr()
             a.hist = hist.data_ptr() if hist is not None else None
             ws_bytes = C.c_size_t()
-            N.check(N.lib().cs_eval_workspace_size(self._h, C.byref(a), C.byref(ws_bytes)))
+            rc = N.lib().cs_eval_workspace_size(self._h, C.byref(a), C.byref(ws_bytes))
+            if rc != N.CS_OK and self.n_grids > 1 and "too large for shared memory" in N.last_error():
+                if per_step or accumulate_hist is not None:
+                    raise ValueError("per-step output and histogram accumulation need every grid's tables in "
+                                     "shared memory at once; split the grids across calls")
+                return self._evaluate_chunked(caps, S, step_seconds=step_seconds, switch_penalty_s=switch_penalty_s,
+                                              check_violations=check_violations, want_hist=want_hist, stream=stream,
+                                              segment_epilogue=segment_epilogue)
+            N.check(rc)
             ws = None
             if ws_bytes.value:
                 ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
@@ -197,6 +205,50 @@ class Tables:
                 a.workspace_bytes = ws_bytes.value
             N.check(N.lib().cs_eval(self._h, C.byref(a), C.c_void_p(_stream_ptr(stream))))
         return EvalResult(self, agg, hist, bins, S, ws)
+
+    def _evaluate_chunked(self, caps, S: int, **kw) -> "EvalResult":
+        """Grids whose merged tables exceed shared memory run as consecutive grid chunks (each a
+        Tables of its own, split in halves until each one's launch plan fits). Every grid's
+        aggregates are independent of the others, so the chunked result is the same; the union-bin
+        histogram is kept per chunk (EvalResult.parts), config histograms per grid are exact."""
+        torch = _torch()
+        key = (float(kw.get("switch_penalty_s", 0.0)) > 0.0, bool(kw.get("want_hist", True)))  # what sizes the plan
+        cache = self.__dict__.setdefault("_chunks", {})
+        if key not in cache:
+            chunks = []
+            todo = [(0, self.n_grids // 2), (self.n_grids // 2, self.n_grids)]  # the whole set does not fit
+            while todo:
+                lo, hi = todo.pop(0)
+                t = Tables.stage(self.grids[lo:hi], self.cap_dtype, batching_mtl=self.batching_mtl,
+                                 multi_tenant_bs=self.multi_tenant_bs)
+                if hi - lo > 1 and not t._plan_fits(caps, S, kw):
+                    mid = (lo + hi) // 2
+                    todo[:0] = [(lo, mid), (mid, hi)]
+                    continue
+                chunks.append((lo, hi, t))
+            cache[key] = chunks
+        agg = torch.empty((caps.shape[0], self.n_grids, 3, 6), dtype=torch.float64, device=caps.device)
+        parts, keep = [], []
+        for lo, hi, t in cache[key]:
+            r = t.evaluate(caps, S, **kw)
+            agg[:, lo:hi] = r.agg
+            parts += [(lo + l2, t2, h2) for l2, t2, h2 in r.parts] if r.parts is not None else [(lo, t, r.hist)]
+            keep.append(r)
+        return EvalResult(self, agg, None, None, S, keep, parts)
+
+    def _plan_fits(self, caps, S: int, kw: dict) -> bool:
+        a = N.EvalArgs()
+        a.caps = caps.data_ptr()
+        a.n_traces = caps.shape[0]
+        a.n_steps = S
+        a.ld = caps.stride(0) if caps.shape[0] > 1 else caps.shape[1]
+        a.step_seconds = int(kw.get("step_seconds", 1))
+        a.switch_penalty_s = float(kw.get("switch_penalty_s", 0.0))
+        a.flags = N.CS_FLAG_CHECK_VIOLATIONS if kw.get("check_violations", True) else 0
+        a.agg = 1
+        a.hist = 1 if kw.get("want_hist", True) else None
+        ws = C.c_size_t()
+        return N.lib().cs_eval_workspace_size(self._h, C.byref(a), C.byref(ws)) == N.CS_OK
 
     def capture(self, caps, n_steps: int | None = None, **kw) -> EvalGraph:
         """evaluate() as a replayable CUDA graph (same arguments; see EvalGraph)."""
@@ -314,6 +366,16 @@ class EvalResult:
     step_bins: "object"  # torch.int16 [T, ld_bins] or None (union bin per step, as uint16)
     n_steps: int
     _ws: "object" = None
+    parts: "object" = None  # chunked runs: [(first grid, chunk Tables, chunk union-bin hist)]
+
+    def config_histograms(self) -> list[list[dict]]:
+        """Per (grid, policy) config histograms {Config or None: steps} (chunked runs included)."""
+        if self.parts is None:
+            return self.tables.config_histograms(self.hist)
+        out = []
+        for _, t, h in self.parts:
+            out += t.config_histograms(h)
+        return out
 
     @property
     def avg_throughput_ips(self):
