@@ -110,7 +110,6 @@ struct EvalParams {
   int32_t wpg, gpc;
   // shared-memory layout (bytes)
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
-  int32_t hstride;  // 32-bit words per histogram entry (1)
 };
 
 namespace {
@@ -952,9 +951,8 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
                        !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
   const size_t bin_bytes = (size_t)6 * U4 * 16;
   const size_t seg_smem = bin_epi ? bin_bytes : a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
-  const int hs = 1;
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
-    size_t gb = a16((size_t)U4 * 4 * hs);
+    size_t gb = a16((size_t)U4 * 4);
     *off_sw = gb;
     gb += pen ? a16((size_t)nsegs * 4) : 0;
     *off_v = gb;
@@ -1060,7 +1058,6 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.hist = reinterpret_cast<unsigned long long*>(a->hist);
   P.wpg = pl.wpg;
   P.gpc = pl.gpc;
-  P.hstride = hs;
   P.U4 = U4;
   P.NSEG = nsegs;
   P.off_vio = (int32_t)lut_b;
