@@ -361,12 +361,13 @@ def main() -> None:
             if rank == 0:
                 out["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:300]}
 
-    if rank == 0 and not args.no_cpu:
-        sample_np = host.numpy()
-        out["cpu_baseline"] = cpu_baseline(grids, sample_np, cfg, args.cpu_budget_s)
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N=1 only
+        out["cpu_baseline"] = cpu_baseline(grids, host.numpy(), cfg, args.cpu_budget_s)
+    if rank == 0:
         # sampled parity on the benchmarked data (bit-exact idle counts, 1e-6 sums)
         from oracle import oracle
 
+        sample_np = host.numpy()
         k = min(8, T)
         avg, idle, en, _ = oracle.simulate_batch(oracle_grids(grids), np.ascontiguousarray(sample_np[:k, :S]),
                                                  cfg["step_seconds"], cfg["penalty"])
@@ -404,6 +405,11 @@ def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total):
     from paper_2306_12247_b200.shard import max_over_ranks
 
     ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps, dev)
+    world = pg.get_world_size() if pg is not None else 1
+    if world > 1:  # whole-job bytes, like the value (every rank moves its own shard)
+        t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+        pg.all_reduce(t)
+        h2d, d2h = int(t[0].item()), int(t[1].item())
     return {"value": T_total * S / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms, "steps": e_steps,
             "path": f"cs_engine_eval_host: pinned host caps, H2D/eval/D2H on 3 streams, {chunk}-trace chunks"}
