@@ -297,6 +297,7 @@ def main() -> None:
     hist_total = int(res.hist.sum())
     assert hist_total == T_total * S, (hist_total, T_total * S)
     assert viol == 0
+    sweep = sweep_summary(tables, res.hist, cfg) if rank == 0 else None
 
     M = len(grids)
     bytes_per_launch = T * S * 4 + T * M * 3 * 48 + tables.n_union_bins * 8
@@ -375,12 +376,36 @@ def main() -> None:
         ok = bool(np.array_equal(g.view(torch.int64)[..., 2].numpy(), idle)
                   and np.allclose(g[..., 0].numpy(), avg, rtol=1e-6, atol=0)
                   and np.allclose(g[..., 1].numpy(), en, rtol=1e-6, atol=0))
+        out["sweep"] = sweep
         out["parity_sample"] = {"traces": k, "ok": ok, "violations": viol,
                                 "bit_exact_avg": bool(np.array_equal(g[..., 0].numpy(), avg))}
     if rank == 0:
         print(json.dumps(out))
     if pg is not None:
         pg.destroy_process_group()
+
+
+def sweep_summary(tables, hist, cfg):
+    """Sweep-level statistics from the reduced union-bin histogram (the one collective): per grid
+    and policy the share of idle steps and the mean per-step throughput over every trace (exact
+    integer counts, fsum on the host). Identical at any GPU count; ``hist_sha256`` makes that
+    checkable across the scaling runs. Penalty-free values (switched steps are per trace)."""
+    import hashlib
+    import math
+
+    h = hist.cpu().numpy()
+    out = {"hist_sha256": hashlib.sha256(h.astype("<i8").tobytes()).hexdigest()[:16], "grids": []}
+    for m, rows in enumerate(tables.config_histograms(h)):
+        g = tables.grids[m]
+        per = {}
+        for p, d in zip(("batching", "multi-tenant", "combination"), rows):
+            n = sum(d.values())
+            thr = math.fsum(c * g.entries[k].throughput_ips for k, c in d.items() if k is not None)
+            per[p] = {"mean_throughput_ips": thr / n, "idle_fraction": d.get(None, 0) / n}
+        out["grids"].append({"model": g.model_name, **per})
+        if m >= 2:
+            break  # first grids only: keeps the line short
+    return out
 
 
 def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total):
