@@ -529,7 +529,7 @@ int32_t ora_select_sampling(const int32_t* mtl, const int32_t* bs, const double*
     ora_mt rng;
     ora_mt_seed(&rng, key, key_len);
     const int64_t k = budget_m;
-    int32_t* picked = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);
+    int32_t* picked = (int32_t*)calloc((size_t)(k > 0 ? k : 1), sizeof(int32_t));
     if (nf <= ora_sample_setsize(k)) {
       int32_t* pool = (int32_t*)malloc(sizeof(int32_t) * (size_t)nf);
       for (int i = 0; i < nf; ++i) pool[i] = i;
