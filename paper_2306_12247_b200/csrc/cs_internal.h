@@ -40,8 +40,8 @@ namespace cs {
 // per-step power check is an OR of that bit, with an exact recount when it is ever set.
 //
 // fp64 (drop-in PowerTrace values): u = clamp(bits, LO, HI); level-1 = (u >> S1) - KBASE;
-// leaf hi16 = base, lo16 = n in {0, 1}; b = base + (n && T64[base] <= u); redirect = 0x8000|s
-// with hi16 = sub-table index.
+// leaf hi16 = base, bit 0 = n in {0, 1}, bit 14 = not proven violation-free; b = base +
+// (n && T64[base] <= u); redirect = 0x8000|s with hi16 = sub-table index.
 // ---------------------------------------------------------------------------------------
 constexpr uint32_t kRedirect32 = 0xFFF00000u;  // fp32 redirect marker (top 12 bits set; leaf bases < 0xFFF0)
 constexpr uint32_t kRedirect = 0x8000u;        // fp64 redirect flag
@@ -82,7 +82,7 @@ CS_HD uint32_t bin_f64(uint64_t bits, int64_t lo, int64_t hi, uint32_t s1, uint6
     e = lut[sub0 + (e >> 16) * kSubFan + (uint32_t)((u >> s) & 15u)];
   }
   uint32_t base = e >> 16;
-  return base + (((e & 0x7FFFu) != 0u && thr64[base] <= u) ? 1u : 0u);
+  return base + (((e & 1u) != 0u && thr64[base] <= u) ? 1u : 0u);
 }
 
 // Clamped bit pattern used by the fp64 violation self-check (same clamp as the lookup).

@@ -639,49 +639,99 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
   return VIO && (flags & 1u);
 }
 
+// fp64 LUT search (cs_internal.h encoding) with thresholds and LUT in shared memory; leaves' bit 14
+// (not proven violation-free) is ORed into flags like the fp32 path's bit 0.
+struct Lut64 {
+  const uint32_t* lut;
+  const uint64_t* thr;
+  int64_t lo, hi;
+  uint64_t kbase;
+  uint32_t s1, sub0;
+
+  __device__ __forceinline__ uint64_t clampu(uint64_t x) const {
+    int64_t si = (int64_t)x;
+    si = si < lo ? lo : si;
+    si = si > hi ? hi : si;
+    return (uint64_t)si;
+  }
+  __device__ __forceinline__ uint32_t entry(uint64_t u) const { return lut[(uint32_t)((u >> s1) - kbase)]; }
+  __device__ __forceinline__ uint32_t resolve(uint32_t e, uint64_t u, uint32_t& flags) const {
+    while (e & kRedirect) e = lut[sub0 + (e >> 16) * kSubFan + (uint32_t)((u >> (e & 0x3Fu)) & 15u)];
+    flags |= e;
+    const uint32_t base = e >> 16;
+    return base + (((e & 1u) != 0u && thr[base] <= u) ? 1u : 0u);
+  }
+  __device__ __forceinline__ uint32_t bin(uint64_t x, uint32_t& flags) const {
+    const uint64_t u = clampu(x);
+    return resolve(entry(u), u, flags);
+  }
+};
+
 template <bool PEN, bool STEP, bool VIO>
-__device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const uint32_t* s_lut, const uint64_t* s_vio,
-                                                uint32_t* h, uint32_t* sw, const uint64_t* s_sig, int64_t t,
-                                                int64_t s0, int64_t s1e, int gtid, int gsize) {
+__device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const Lut64& L, uint32_t* h, uint32_t* sw,
+                                                const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
+                                                int gsize) {
   const DevTables& tb = P.tb;
   const int U = tb.U, M = tb.M;
   const int32_t* s_segoff = reinterpret_cast<const int32_t*>(s_sig + (size_t)M * U);
   const unsigned long long* row = reinterpret_cast<const unsigned long long*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
-  bool bad = false;
-  auto bin = [&](uint64_t x) {
-    return bin_f64(x, P.lv.lo, P.lv.hi, P.lv.shift1, P.lv.kbase, P.lv.sub0, s_lut, P.lv.thr64);
+  uint32_t flags = 0;
+  auto switches = [&](uint32_t cb, uint32_t pb) {
+    if (cb != pb)
+      for (int m = 0; m < M; ++m) {
+        const uint64_t sc = s_sig[(size_t)m * U + cb], xo = sc ^ s_sig[(size_t)m * U + pb];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+          if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[s_segoff[m * 3 + p] + (int)((sc >> (16 * p)) & 0xFFFFull)], 1u);
+      }
   };
-  auto one = [&](uint64_t x, int64_t gi, uint32_t b) {
-    atomicAdd(&h[b], 1u);
-    if (VIO) bad |= clamp_bits_f64(x, P.lv.lo, P.lv.hi) < s_vio[b];
+  // 4 caps (two 128-bit loads) per lane and pass: entries first, then the leaves, for ILP
+  const int nq = n >> 2;
+  for (int q = gtid; q < nq; q += gsize) {
+    const uint4 ra = ldg_stream(vrow + (size_t)q * 32), rb = ldg_stream(vrow + (size_t)q * 32 + 16);
+    uint64_t u[4] = {((uint64_t)ra.y << 32) | ra.x, ((uint64_t)ra.w << 32) | ra.z, ((uint64_t)rb.y << 32) | rb.x,
+                     ((uint64_t)rb.w << 32) | rb.z};
+    uint32_t e[4], b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) u[k] = L.clampu(u[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = L.entry(u[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = L.resolve(e[k], u[k], flags);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) atomicAdd(&h[b[k]], 1u);
+    const int64_t gi = s0 + 4 * (int64_t)q;
     if (PEN) {
-      const uint32_t pb = gi > 0 ? bin(__ldg(row + gi - 1)) : b;
-      if (b != pb)
-        for (int m = 0; m < M; ++m) {
-          const uint64_t xo = s_sig[(size_t)m * U + b] ^ s_sig[(size_t)m * U + pb];
-          for (int p = 0; p < 3; ++p)
-            if ((xo >> (16 * p)) & 0xFFFFull)
-              atomicAdd(&sw[s_segoff[m * 3 + p] + (int)((s_sig[(size_t)m * U + b] >> (16 * p)) & 0xFFFFull)], 1u);
-        }
+      uint32_t pb = b[0];  // step 0 is never penalised (sim.py:119)
+      if (gi > 0) {
+        uint32_t dummy = 0;
+        pb = L.bin(__ldg(row + gi - 1), dummy);
+      }
+      switches(b[0], pb);
+      switches(b[1], b[0]);
+      switches(b[2], b[1]);
+      switches(b[3], b[2]);
+    }
+    if (STEP) {
+      uint2 o;
+      o.x = (b[0] & 0xFFFFu) | (b[1] << 16);
+      o.y = (b[2] & 0xFFFFu) | (b[3] << 16);
+      *reinterpret_cast<uint2*>(P.step_bins + t * P.ld_bins + gi) = o;
+    }
+  }
+  for (int i = 4 * nq + gtid; i < n; i += gsize) {  // tail (< 4 caps at the end of the segment)
+    const int64_t gi = s0 + i;
+    const uint32_t b = L.bin(__ldg(row + gi), flags);
+    atomicAdd(&h[b], 1u);
+    if (PEN) {
+      uint32_t dummy = 0;
+      switches(b, gi > 0 ? L.bin(__ldg(row + gi - 1), dummy) : b);
     }
     if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
-  };
-  const int nvf = n >> 1;
-  for (int v = gtid; v < nvf; v += gsize) {
-    const uint4 r = ldg_stream(vrow + (size_t)v * 16);
-    const uint64_t x0 = ((uint64_t)r.y << 32) | r.x, x1 = ((uint64_t)r.w << 32) | r.z;
-    const int64_t gi = s0 + 2 * (int64_t)v;
-    one(x0, gi, bin(x0));
-    one(x1, gi + 1, bin(x1));
   }
-  if ((n & 1) && gtid == 0) {
-    const int64_t gi = s1e - 1;
-    const uint64_t x = __ldg(row + gi);
-    one(x, gi, bin(x));
-  }
-  return bad;
+  return VIO && (flags & 0x4000u);
 }
 
 template <typename CapT, bool PEN, bool STEP, bool VIO>
@@ -694,10 +744,10 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   // ---- N1: stage the tables into shared memory once per CTA ----
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
   for (int i = threadIdx.x; i < P.n_lut; i += blockDim.x) s_lut[i] = __ldg(P.lv.lut + i);
-  // fp64 tables: violation floors per union bin (fp32 tables carry the proof in the LUT leaves)
-  uint64_t* s_vio = reinterpret_cast<uint64_t*>(smem + P.off_vio);
-  if (!F32 && VIO)
-    for (int i = threadIdx.x; i < U; i += blockDim.x) s_vio[i] = __ldg(tb.vio + i);
+  // fp64 tables: the thresholds the leaves compare against (fp32 leaves need none)
+  uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem + P.off_vio);
+  if (!F32)
+    for (int i = threadIdx.x; i < U - 1; i += blockDim.x) s_thr[i] = __ldg(P.lv.thr64 + i);
   uint64_t* s_sig = reinterpret_cast<uint64_t*>(smem + P.off_sig);
   int32_t* s_segoff = reinterpret_cast<int32_t*>(s_sig + (size_t)M * U);  // [M*3+1] (PEN)
   if (PEN) {
@@ -747,6 +797,14 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag
   __syncthreads();
 
+  Lut64 L64;
+  L64.lut = s_lut;
+  L64.thr = s_thr;
+  L64.lo = P.lv.lo;
+  L64.hi = P.lv.hi;
+  L64.kbase = P.lv.kbase;
+  L64.s1 = P.lv.shift1;
+  L64.sub0 = P.lv.sub0;
   Lut32 L;
   L.lut = s_lut;
   L.kb = (int32_t)P.lv.kbase;
@@ -765,7 +823,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     if constexpr (F32)
       bad = run_segment_f32<PEN, STEP, VIO>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     else
-      bad = run_segment_f64<PEN, STEP, VIO>(P, s_lut, s_vio, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+      bad = run_segment_f64<PEN, STEP, VIO>(P, L64, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     if (VIO && bad) atomicOr(&vcnt[M * 3], 1u);
     group_sync(gid_local, gsize);
     if (VIO && vcnt[M * 3]) {  // never taken when the tables are right: exact recount
@@ -937,7 +995,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int nsm = sm_count(dev);
   const size_t lut_bytes = a16((size_t)t.lut.size() * 4);
-  const size_t vio_bytes = (vio && !f32) ? a16((size_t)U * 8) : 0;
+  const size_t vio_bytes = !f32 ? a16((size_t)U * 8) : 0;  // fp64: the thresholds (s_thr)
   const int U4 = (U + 3) & ~3;
   const int nsegs = (int)(t.seg.size() / 4);
   const size_t sig_bytes = pen ? a16((size_t)M * U * 8 + (size_t)(M * 3 + 1) * 4) : 0;

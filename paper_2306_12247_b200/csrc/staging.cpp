@@ -109,9 +109,9 @@ struct LutBuilder {
         if (tl == 0) return ((base + 1) << 16) | flag(start, base + 1, false, 0);  // threshold on the start
         return (base << 16) | ((0x4000u - tl) << 2) | flag(start, base, true, T[base]);
       }
-    } else {
-      if (n == 0) return base << 16;
-      if (n == 1) return (base << 16) | 1u;
+    } else {  // fp64: bit 14 marks a leaf not proven violation-free (the kernel ORs it)
+      if (n == 0) return (base << 16) | (flag(start, base, false, 0) << 14);
+      if (n == 1) return (base << 16) | 1u | (flag(start, base, true, T[base]) << 14);
     }
     uint32_t ns = s >= 4 ? s - 4 : 0;
     uint32_t id = n_sub++;
@@ -184,7 +184,7 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
   const uint32_t s = best_s;
   uint64_t kb, nb;
   if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
-  LutBuilder lbld(T, f32, f32 ? &t.vio : nullptr);
+  LutBuilder lbld(T, f32, &t.vio);
   out.kbase = kb;
   std::vector<uint32_t> level1(nb);
   for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
