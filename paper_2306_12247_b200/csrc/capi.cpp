@@ -268,10 +268,17 @@ int cs_tables_lookup_host_lut(const cs_tables* tp, const void* caps, int64_t n, 
   if (which == 0) return cs_tables_lookup_host(tp, caps, n, bins_out);
   if (which != 1 || t.lut_big.lut.empty()) return fail(CS_E_INVALID, "no such LUT");
   const Tables::Lut& L = t.lut_big;
-  const uint32_t* c = reinterpret_cast<const uint32_t*>(caps);
-  for (int64_t i = 0; i < n; ++i)
-    bins_out[i] = (int32_t)cs::bin_f32(c[i], L.shift1, (int32_t)L.kbase, (int32_t)L.n_level1, L.n_level1,
-                                       L.lut.data());
+  if (t.cap_dtype == CS_CAP_F32) {
+    const uint32_t* c = reinterpret_cast<const uint32_t*>(caps);
+    for (int64_t i = 0; i < n; ++i)
+      bins_out[i] = (int32_t)cs::bin_f32(c[i], L.shift1, (int32_t)L.kbase, (int32_t)L.n_level1, L.n_level1,
+                                         L.lut.data());
+  } else {
+    const uint64_t* c = reinterpret_cast<const uint64_t*>(caps);
+    for (int64_t i = 0; i < n; ++i)
+      bins_out[i] = (int32_t)cs::bin_f64(c[i], t.lo, t.hi, L.shift1, L.kbase, L.n_level1, L.lut.data(),
+                                         t.thresholds.data());
+  }
   return CS_OK;
 }
 
