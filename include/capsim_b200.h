@@ -208,6 +208,16 @@ int cs_select_sampling(const cs_tables* t, int32_t grid, const double* caps_dev,
                        int64_t ld, int64_t budget_m, int64_t rounds_r, uint64_t seed_lo, int64_t seed_hi,
                        int32_t* out_entry_dev, int32_t* out_count_dev, void* stream);
 
+/* _aggregate (sim.py:104-127) of per-step entry selections on the device (the summary reports of
+ * simulate_many with a sampling policy): entry_dev int32 [n_traces][ld] caller entry index or -1
+ * (idle); values_dev f64 [3][n_entries + 1][2] per entry {hi, lo} of thr, penalised thr
+ * (thr * (1 - penalty_frac)) and energy ((power or idle power) * step / 3600), index n_entries =
+ * idle, each split so that the sum of hi is exact; outputs per trace the
+ * average throughput (fsum(ips) / n), the energy and the idle-step count. */
+int cs_entries_aggregate(const int32_t* entry_dev, int64_t n_traces, int64_t n_steps, int64_t ld,
+                         const double* values_dev, int32_t n_entries, double penalty_frac, double* avg_dev,
+                         double* energy_dev, int64_t* idle_dev, void* stream);
+
 /* ---- synthetic traces for benchmarks (counter-based, keyed by (seed, global trace id)) ---- */
 #define CS_TRACE_SOLAR 0
 #define CS_TRACE_WIND 1

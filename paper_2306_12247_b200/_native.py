@@ -38,7 +38,7 @@ EXPORTS = (
     "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches", "cs_eval_last_plan",
     "cs_select_caps", "cs_feasible_caps",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
-    "cs_replay", "cs_generate_traces", "cs_select_sampling",
+    "cs_replay", "cs_generate_traces", "cs_select_sampling", "cs_entries_aggregate",
     "cs_traces_parse_files", "cs_traces_parse_text", "cs_traces_info", "cs_traces_copy", "cs_traces_pack",
     "cs_traces_destroy",
 )
@@ -165,6 +165,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_generate_traces": ([vp, i64, i64, i64, i64, i32, i32, C.c_float, C.c_uint64, vp], C.c_int),
         "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),
         "cs_select_sampling": ([vp, i32, vp, i64, i64, i64, i64, i64, C.c_uint64, i64, vp, vp, vp], C.c_int),
+        "cs_entries_aggregate": ([vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp], C.c_int),
         "cs_traces_parse_files": ([P(C.c_char_p), i32, i64, i32, i32, P(vp)], C.c_int),
         "cs_traces_parse_text": ([C.c_char_p, i64, i64, i32, P(vp)], C.c_int),
         "cs_traces_info": ([vp, i32, P(TraceInfo)], C.c_int),

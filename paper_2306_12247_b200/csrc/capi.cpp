@@ -11,6 +11,12 @@
 
 #include "cs_internal.h"
 
+#include <vector_types.h>
+namespace cs {
+std::string launch_entries_agg(const int32_t* ent, int64_t T, int64_t S, int64_t ld, const double2* vals, int n,
+                               double pf, double* avg, double* energy, int64_t* idle, cudaStream_t st);
+}  // namespace cs
+
 namespace cs {
 std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, cudaStream_t st);
 std::string eval_workspace(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, size_t* bytes);
@@ -434,6 +440,19 @@ int cs_select_sampling(const cs_tables* tp, int32_t grid, const double* caps_dev
   std::string err = cs::launch_sampling(d->view, grid, caps_dev, n_traces, n_steps, ld, budget_m, rounds_r, seed_lo,
                                         seed_hi, out_entry_dev, out_count_dev, (int)n_entries, sms,
                                         reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+int cs_entries_aggregate(const int32_t* entry_dev, int64_t n_traces, int64_t n_steps, int64_t ld,
+                         const double* values_dev, int32_t n_entries, double penalty_frac, double* avg_dev,
+                         double* energy_dev, int64_t* idle_dev, void* stream) {
+  if (n_traces < 0 || n_steps < 1 || ld < n_steps || n_entries < 1 || !(penalty_frac >= 0.0 && penalty_frac <= 1.0) ||
+      (n_traces > 0 && (!entry_dev || !values_dev || !avg_dev || !energy_dev || !idle_dev)))
+    return fail(CS_E_INVALID, "bad aggregate arguments");
+  std::string err = cs::launch_entries_agg(entry_dev, n_traces, n_steps, ld,
+                                           reinterpret_cast<const double2*>(values_dev), n_entries, penalty_frac,
+                                           avg_dev, energy_dev, idle_dev, reinterpret_cast<cudaStream_t>(stream));
   if (!err.empty()) return fail(CS_E_CUDA, err);
   return CS_OK;
 }

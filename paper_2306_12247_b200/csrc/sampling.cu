@@ -220,4 +220,56 @@ std::string launch_sampling(const DevTables& v, int g, const double* caps, int64
   return std::string();
 }
 
+// _aggregate (sim.py:104-127) over per-step entry selections (the sampling selector's output):
+// one warp per trace. Every per-step value comes from a small per-entry table whose values the
+// host pre-split into {hi, lo} (hi on a quantum grid so that the sum of hi is exact in fp64, like
+// prep_kernel's split), so the result equals the reference's math.fsum up to the lo parts.
+//   vals[j * (n + 1) + e], j = 0 thr, 1 penalised thr (thr * (1 - pf)), 2 energy; e = n: idle
+__global__ void __launch_bounds__(256) entries_agg_kernel(const int32_t* ent, int64_t T, int64_t S, int64_t ld,
+                                                          const double2* vals, int n, double pf, double* avg,
+                                                          double* energy, int64_t* idle) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int32_t* row = ent + t * ld;
+  double th = 0.0, tl = 0.0, eh = 0.0, el = 0.0;
+  uint32_t id = 0;
+  for (int64_t i = lane; i < S; i += 32) {
+    const int32_t e = row[i];
+    const int k = e < 0 ? n : e;
+    const bool sw = pf > 0.0 && i > 0 && row[i - 1] != e;  // sim.py:119 (None vs config counts)
+    const double2 v = vals[(sw ? 1 : 0) * (n + 1) + k];
+    const double2 w = vals[2 * (n + 1) + k];
+    th = __dadd_rn(th, v.x);
+    tl = __dadd_rn(tl, v.y);
+    eh = __dadd_rn(eh, w.x);
+    el = __dadd_rn(el, w.y);
+    id += e < 0 ? 1u : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    th = __dadd_rn(th, __shfl_xor_sync(0xffffffffu, th, o));
+    tl = __dadd_rn(tl, __shfl_xor_sync(0xffffffffu, tl, o));
+    eh = __dadd_rn(eh, __shfl_xor_sync(0xffffffffu, eh, o));
+    el = __dadd_rn(el, __shfl_xor_sync(0xffffffffu, el, o));
+  }
+  id = __reduce_add_sync(0xffffffffu, id);
+  if (lane == 0) {
+    avg[t] = __ddiv_rn(__dadd_rn(th, tl), (double)S);  // fsum(ips) / n
+    energy[t] = __dadd_rn(eh, el);
+    idle[t] = id;
+  }
+}
+
+std::string launch_entries_agg(const int32_t* ent, int64_t T, int64_t S, int64_t ld, const double2* vals, int n,
+                               double pf, double* avg, double* energy, int64_t* idle, cudaStream_t st) {
+  if (T <= 0) return std::string();
+  const int64_t blocks = (T + 7) / 8;
+  entries_agg_kernel<<<(unsigned)blocks, 256, 0, st>>>(ent, T, S, ld, vals, n, pf, avg, energy, idle);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return std::string("CUDA error: ") + cudaGetErrorString(e);
+  set_last_launches(1);
+  return std::string();
+}
+
 }  // namespace cs

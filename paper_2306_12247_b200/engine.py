@@ -302,6 +302,40 @@ class Tables:
                                                cnt.data_ptr(), C.c_void_p(_stream_ptr(None))))
         return ent, cnt
 
+    def aggregate_entries(self, grid_index: int, entries_dev, n_steps: int, *, step_seconds: int,
+                          switch_penalty_s: float = 0.0):
+        """_aggregate (sim.py:104-127) of per-step entry selections ``entries_dev`` int32 [T, ld]
+        (caller entry index, -1 idle) on the device: (avg_throughput_ips f64 [T], energy_proxy_wh
+        f64 [T], idle_steps int64 [T]). Values are split {hi, lo} so the sums of hi are exact."""
+        torch = _torch()
+        g = self.grids[grid_index]
+        _, _, _, thr, pw = grid_arrays(g)
+        idle_pw = g.gpu_idle_power_w if g.gpu_idle_power_w is not None else 0.0
+        step = float(step_seconds)
+        pf = min(float(switch_penalty_s), step) / step
+        thr1 = np.append(thr, 0.0)
+        vals = [thr1, thr1 * (1.0 - pf), np.append(pw, idle_pw) * step / 3600.0]  # sim.py:111,120,122
+        L = 52
+        while L > 1 and float(n_steps) >= 2.0 ** (53 - L):
+            L -= 1
+        table = np.zeros((3, thr1.shape[0], 2))
+        for j, v in enumerate(vals):
+            ref = v if j != 1 else vals[0]  # thr and penalised thr share the quantum
+            e = np.frexp(max(float(ref.max()), 0.0) or 1.0)[1] - L
+            hi = np.ldexp(np.floor(np.ldexp(v, -e)), e)
+            table[j, :, 0], table[j, :, 1] = hi, v - hi
+        T = entries_dev.shape[0]
+        dev = entries_dev.device
+        tv = torch.from_numpy(table).to(dev)
+        avg = torch.empty(T, dtype=torch.float64, device=dev)
+        en = torch.empty(T, dtype=torch.float64, device=dev)
+        idle = torch.empty(T, dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            N.check(N.lib().cs_entries_aggregate(entries_dev.data_ptr(), T, int(n_steps), entries_dev.stride(0),
+                                                 tv.data_ptr(), int(thr.shape[0]), pf, avg.data_ptr(), en.data_ptr(),
+                                                 idle.data_ptr(), C.c_void_p(_stream_ptr(None))))
+        return avg, en, idle
+
     def feasible_caps(self, grid_index: int, policy: int, caps_dev):
         """feasible_set for many caps: warp-per-cap ballot bitmask (policy.py:151-169)."""
         torch = _torch()

@@ -108,3 +108,28 @@ def test_sampling_errors(cs):
     assert cs.select_sampling(g1, 4, 2, float("nan"), 0).config is None
     big = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
     assert cs.select_sampling(big, 5000, 0, 200.0, 0) == cs.select_config(big, cs.COMBINATION, 200.0)
+
+
+def test_device_entry_aggregate_matches_fsum(cs):
+    """cs_entries_aggregate (simulate_many's sampling summaries) vs the reference's _aggregate
+    restated on the host with math.fsum, over random per-step selections and penalties."""
+    import torch
+
+    from paper_2306_12247_b200.sim import _sampling_aggregate
+
+    g = cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128, noise_pct=2.0, seed=9))
+    tables = cs.Tables.stage([g], "f64")
+    rng = np.random.default_rng(17)
+    n = len(g.entries)
+    for S, pen, step in ((1, 0.0, 60), (777, 0.0, 60), (10080, 20.0, 60), (5000, 7200.0, 3600)):
+        ent = rng.integers(-1, n, size=(64, S)).astype(np.int32)
+        ent[:8] = np.repeat(rng.integers(-1, n, size=(8, 1)), S, axis=1)  # constant rows
+        avg, en, idle = tables.aggregate_entries(0, torch.from_numpy(ent).cuda(), S, step_seconds=step,
+                                                 switch_penalty_s=pen)
+        avg, en, idle = avg.cpu().numpy(), en.cpu().numpy(), idle.cpu().numpy()
+        want = [_sampling_aggregate(g, ent[t], step, float(g.gpu_idle_power_w or 0.0), pen) for t in range(64)]
+        wa = np.array([w[0] for w in want])
+        we = np.array([w[2] for w in want])
+        assert np.array_equal(idle, [w[1] for w in want])
+        assert np.allclose(avg, wa, rtol=1e-12, atol=0) and np.allclose(en, we, rtol=1e-12, atol=0)
+        assert np.mean(avg == wa) >= 0.95 and np.mean(en == we) >= 0.95

@@ -45,3 +45,10 @@ for m, r in ((8, 2), (64, 2)):
     dt = timed(lambda: cs.simulate_many([g], traces, kinds=[kind]), reps=1)
     n = len(traces) * S
     print(f"sampling(m={m},r={r}): {len(traces)}x{S} in {dt * 1e3:.1f} ms -> {n / dt / 1e6:.1f} M steps/s")
+
+# the sampling kernel alone (per-step entries on the device, no host aggregation)
+tables = cs.Tables.stage([g], "f64")
+cd = torch.from_numpy(np.ascontiguousarray(caps[:256])).cuda()
+for m in (8, 64):
+    dt = timed(lambda: tables.select_sampling(0, cd, S, m, 2, 0))
+    print(f"sampling kernel (m={m},r=2): 256x{S} in {dt * 1e3:.1f} ms -> {256 * S / dt / 1e6:.1f} M steps/s")
