@@ -355,7 +355,7 @@ def main() -> None:
     torch.cuda.empty_cache()
     if not args.no_e2e:
         try:
-            e2e = run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total)
+            e2e = run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=res.agg[:64])
             if rank == 0:
                 out["e2e"] = e2e
         except Exception as exc:  # keep the device-side line even if the host path fails
@@ -408,7 +408,7 @@ def sweep_summary(tables, hist, cfg):
     return out
 
 
-def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total):
+def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=None):
     """cs_engine_eval_host over pinned host caps: every step copies the caps H2D and the
     per-trace aggregates + histogram D2H inside the timed region (wall clock around the
     blocking C call, max over ranks)."""
@@ -430,13 +430,16 @@ def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total):
     from paper_2306_12247_b200.shard import max_over_ranks
 
     ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps, dev)
+    # the host path must reproduce the device path's aggregates exactly (same kernel, same data)
+    k = min(64, T)
+    same = bool(torch.equal(agg_h[:k], ref_agg[:k].cpu())) if ref_agg is not None else None
     world = pg.get_world_size() if pg is not None else 1
     if world > 1:  # whole-job bytes, like the value (every rank moves its own shard)
         t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device=dev)
         pg.all_reduce(t)
         h2d, d2h = int(t[0].item()), int(t[1].item())
     return {"value": T_total * S / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": e_steps,
+            "ms_per_step": ms, "steps": e_steps, "matches_device_path": same,
             "path": f"cs_engine_eval_host: pinned host caps, H2D/eval/D2H on 3 streams, {chunk}-trace chunks"}
 
 
