@@ -226,6 +226,18 @@ int cs_entries_aggregate(const int32_t* entry_dev, int64_t n_traces, int64_t n_s
 int cs_generate_traces(float* caps_dev, int64_t n_traces, int64_t n_steps, int64_t ld, int64_t first_trace_id,
                        int32_t step_seconds, int32_t kind, float peak_w, uint64_t seed, void* stream);
 
+/* ---- low-latency per-cap queries from host memory (the scalar drop-in API) ----
+ * caps_host: n fp64 caps. CS_QUERY_BINS: out int32 [n] union bin per cap (PolicyIndex.select,
+ * policy.py:136-148, decoded per regime with cs_tables_grid_bins); CS_QUERY_SELECT: out int32 [n]
+ * entry or -1, out2 int64 [n] feasible_count (select_config, policy.py:172-188);
+ * CS_QUERY_FEASIBLE: out uint32 [n][ceil(entries/32)] bitmask (feasible_set, policy.py:151-169).
+ * One H2D, one kernel, one D2H and one sync per call through per-thread pinned staging buffers. */
+#define CS_QUERY_BINS 0
+#define CS_QUERY_SELECT 1
+#define CS_QUERY_FEASIBLE 2
+int cs_query_host(const cs_tables* t, int32_t query, int32_t grid, int32_t policy, const double* caps_host,
+                  int64_t n, void* out_host, void* out2_host);
+
 /* ---- trace ingestion fast path (load_trace, trace.py:87-169) ----
  * CSV text -> fp64 samples on the host with the reference's rules (header, blank rows, 2
  * fields, ISO-8601 UTC timestamps on the step grid, finite non-negative capacities, whole-step

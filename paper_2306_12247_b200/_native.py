@@ -28,6 +28,10 @@ CS_FLAG_CHECK_VIOLATIONS = 1
 CS_FLAG_ACCUMULATE_HIST = 2
 CS_FLAG_SEGMENT_EPILOGUE = 4
 
+CS_QUERY_BINS = 0
+CS_QUERY_SELECT = 1
+CS_QUERY_FEASIBLE = 2
+
 TRACE_KINDS = {"solar": 0, "wind": 1, "mixed": 2, "iid": 3}
 
 # Every symbol declared in include/capsim_b200.h (checked by tests/test_native_abi.py).
@@ -36,7 +40,7 @@ EXPORTS = (
     "cs_tables_create", "cs_tables_destroy", "cs_tables_get_info", "cs_tables_grid_bins",
     "cs_tables_union_map", "cs_tables_lookup_host", "cs_tables_lookup_host_lut", "cs_tables_upload",
     "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches", "cs_eval_last_plan",
-    "cs_select_caps", "cs_feasible_caps",
+    "cs_select_caps", "cs_feasible_caps", "cs_query_host",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
     "cs_replay", "cs_generate_traces", "cs_select_sampling", "cs_entries_aggregate",
     "cs_traces_parse_files", "cs_traces_parse_text", "cs_traces_info", "cs_traces_copy", "cs_traces_pack",
@@ -165,6 +169,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_generate_traces": ([vp, i64, i64, i64, i64, i32, i32, C.c_float, C.c_uint64, vp], C.c_int),
         "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),
         "cs_select_sampling": ([vp, i32, vp, i64, i64, i64, i64, i64, C.c_uint64, i64, vp, vp, vp], C.c_int),
+        "cs_query_host": ([vp, i32, i32, i32, vp, i64, vp, vp], C.c_int),
         "cs_entries_aggregate": ([vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp], C.c_int),
         "cs_traces_parse_files": ([P(C.c_char_p), i32, i64, i32, i32, P(vp)], C.c_int),
         "cs_traces_parse_text": ([C.c_char_p, i64, i64, i32, P(vp)], C.c_int),

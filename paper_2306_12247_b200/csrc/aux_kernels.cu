@@ -172,6 +172,21 @@ __global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_
   }
 }
 
+// PolicyIndex.select (policy.py:136-148): union bin of each cap through the staged LUT (global
+// memory; a handful of caps per launch). The caller decodes the bin per regime on the host.
+__global__ void lookup_kernel(const DevTables tb, const double* __restrict__ caps, int64_t n,
+                              int32_t* __restrict__ bins) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (tb.cap_dtype == CS_CAP_F64) {
+    bins[i] = (int32_t)bin_f64((uint64_t)__double_as_longlong(caps[i]), tb.lv.lo, tb.lv.hi, tb.lv.shift1,
+                               tb.lv.kbase, tb.lv.sub0, tb.lv.lut, tb.lv.thr64);
+  } else {
+    bins[i] = (int32_t)bin_f32(__float_as_uint((float)caps[i]), tb.lv.shift1, (int32_t)tb.lv.kbase, tb.n_level1,
+                               tb.lv.sub0, tb.lv.lut);
+  }
+}
+
 // ----------------------------------------------------------------------------------------
 // host-side launchers
 // ----------------------------------------------------------------------------------------
@@ -183,6 +198,14 @@ std::string launch_select(const DevTables& v, int g, int p, const double* caps, 
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 32);
   select_kernel<<<(unsigned)blocks, threads, 0, st>>>(v, g, p, caps, n, sel, cnt);
+  CS_CUDA_TRY(cudaGetLastError());
+  set_last_launches(1);
+  return std::string();
+}
+
+std::string launch_lookup(const DevTables& v, const double* caps, int64_t n, int32_t* bins, cudaStream_t st) {
+  if (n <= 0) return std::string();
+  lookup_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(v, caps, n, bins);
   CS_CUDA_TRY(cudaGetLastError());
   set_last_launches(1);
   return std::string();

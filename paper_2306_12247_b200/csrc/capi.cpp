@@ -13,6 +13,9 @@
 
 #include <vector_types.h>
 namespace cs {
+std::string launch_lookup(const DevTables& v, const double* caps, int64_t n, int32_t* bins, cudaStream_t st);
+}  // namespace cs
+namespace cs {
 std::string launch_entries_agg(const int32_t* ent, int64_t T, int64_t S, int64_t ld, const double2* vals, int n,
                                double pf, double* avg, double* energy, int64_t* idle, cudaStream_t st);
 }  // namespace cs
@@ -381,6 +384,82 @@ int cs_select_caps(const cs_tables* tp, int32_t grid, int32_t policy, const doub
   std::string err = cs::launch_select(d->view, grid, policy, caps_dev, n, sel_dev, count_dev,
                                       reinterpret_cast<cudaStream_t>(stream));
   if (!err.empty()) return fail(CS_E_CUDA, err);
+  return CS_OK;
+}
+
+// Low-latency host-buffer queries for the per-cap API: the caps go through a per-thread pinned
+// staging buffer on a per-thread stream (one H2D, one launch, one D2H, one sync per call).
+namespace {
+struct QueryStage {
+  int device = -1;
+  cudaStream_t st = nullptr;
+  unsigned char* hpin = nullptr;
+  unsigned char* dbuf = nullptr;
+  size_t cap = 0;  // (not freed at thread exit: the CUDA runtime may already be torn down)
+};
+thread_local QueryStage g_qs;
+
+int query_stage(int dev, size_t bytes) {
+  if (g_qs.device != dev) {
+    if (g_qs.st) cudaStreamDestroy(g_qs.st), g_qs.st = nullptr;
+    if (g_qs.hpin) cudaFreeHost(g_qs.hpin), g_qs.hpin = nullptr;
+    if (g_qs.dbuf) cudaFree(g_qs.dbuf), g_qs.dbuf = nullptr;
+    g_qs.cap = 0;
+    CS_CUDA_RET(cudaStreamCreateWithFlags(&g_qs.st, cudaStreamNonBlocking));
+    g_qs.device = dev;
+  }
+  if (g_qs.cap < bytes) {
+    size_t c = std::max<size_t>(bytes, 1 << 16);
+    if (g_qs.hpin) cudaFreeHost(g_qs.hpin), g_qs.hpin = nullptr;
+    if (g_qs.dbuf) cudaFree(g_qs.dbuf), g_qs.dbuf = nullptr;
+    g_qs.cap = 0;
+    CS_CUDA_RET(cudaMallocHost(&g_qs.hpin, c));
+    CS_CUDA_RET(cudaMalloc(&g_qs.dbuf, c));
+    g_qs.cap = c;
+  }
+  return CS_OK;
+}
+}  // namespace
+
+int cs_query_host(const cs_tables* tp, int32_t query, int32_t grid, int32_t policy, const double* caps_host,
+                  int64_t n, void* out_host, void* out2_host) {
+  if (n < 0 || (n > 0 && (!caps_host || !out_host))) return fail(CS_E_INVALID, "null argument");
+  if (n == 0) return CS_OK;
+  Tables::Dev* d = nullptr;
+  int dev = 0;
+  int rc = cs::current_view(tp, &d, &dev);
+  if (rc) return rc;
+  const Tables& t = *reinterpret_cast<const Tables*>(tp);
+  if (query != CS_QUERY_BINS && (grid < 0 || grid >= d->view.M || policy < 0 || policy > 2))
+    return fail(CS_E_INVALID, "grid/policy out of range");
+  const int64_t ne = query == CS_QUERY_FEASIBLE ? t.e_off[grid + 1] - t.e_off[grid] : 0;
+  const int64_t words = (ne + 31) / 32;
+  size_t out_b = 0, out2_b = 0;
+  if (query == CS_QUERY_BINS) out_b = (size_t)n * 4;
+  else if (query == CS_QUERY_SELECT) out_b = (size_t)n * 4, out2_b = (size_t)n * 8;
+  else if (query == CS_QUERY_FEASIBLE) out_b = (size_t)n * words * 4;
+  else return fail(CS_E_INVALID, "unknown query");
+  auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t in_b = a16((size_t)n * 8), o1 = a16(out_b);
+  rc = query_stage(dev, in_b + o1 + a16(out2_b));
+  if (rc) return rc;
+  std::memcpy(g_qs.hpin, caps_host, (size_t)n * 8);
+  cudaStream_t st = g_qs.st;
+  CS_CUDA_RET(cudaMemcpyAsync(g_qs.dbuf, g_qs.hpin, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  const double* cd = reinterpret_cast<const double*>(g_qs.dbuf);
+  std::string err;
+  if (query == CS_QUERY_BINS)
+    err = cs::launch_lookup(d->view, cd, n, reinterpret_cast<int32_t*>(g_qs.dbuf + in_b), st);
+  else if (query == CS_QUERY_SELECT)
+    err = cs::launch_select(d->view, grid, policy, cd, n, reinterpret_cast<int32_t*>(g_qs.dbuf + in_b),
+                            reinterpret_cast<int64_t*>(g_qs.dbuf + in_b + o1), st);
+  else
+    err = cs::launch_feasible(d->view, grid, policy, cd, n, reinterpret_cast<uint32_t*>(g_qs.dbuf + in_b), st);
+  if (!err.empty()) return fail(CS_E_CUDA, err);
+  CS_CUDA_RET(cudaMemcpyAsync(g_qs.hpin + in_b, g_qs.dbuf + in_b, o1 + a16(out2_b), cudaMemcpyDeviceToHost, st));
+  CS_CUDA_RET(cudaStreamSynchronize(st));
+  std::memcpy(out_host, g_qs.hpin + in_b, out_b);
+  if (out2_b && out2_host) std::memcpy(out2_host, g_qs.hpin + in_b + o1, out2_b);
   return CS_OK;
 }
 

@@ -336,6 +336,24 @@ class Tables:
                                                  idle.data_ptr(), C.c_void_p(_stream_ptr(None))))
         return avg, en, idle
 
+    def query(self, kind: int, caps, grid_index: int = 0, policy: int = 0):
+        """Low-latency per-cap query from host memory (cs_query_host): one H2D, one kernel, one
+        D2H and a sync. kind: N.CS_QUERY_BINS -> union bins int32 [n]; CS_QUERY_SELECT ->
+        (entry int32 [n], feasible_count int64 [n]); CS_QUERY_FEASIBLE -> uint32 [n, words]."""
+        require_device()
+        c = np.ascontiguousarray(caps, dtype=np.float64)
+        n = c.shape[0]
+        out2 = None
+        if kind == N.CS_QUERY_BINS:
+            out = np.empty(n, np.int32)
+        elif kind == N.CS_QUERY_SELECT:
+            out, out2 = np.empty(n, np.int32), np.empty(n, np.int64)
+        else:
+            out = np.empty((n, (len(self.grids[grid_index].entries) + 31) // 32), np.uint32)
+        N.check(N.lib().cs_query_host(self._h, int(kind), int(grid_index), int(policy), c.ctypes.data, n,
+                                      out.ctypes.data, None if out2 is None else out2.ctypes.data))
+        return out if out2 is None else (out, out2)
+
     def feasible_caps(self, grid_index: int, policy: int, caps_dev):
         """feasible_set for many caps: warp-per-cap ballot bitmask (policy.py:151-169)."""
         torch = _torch()

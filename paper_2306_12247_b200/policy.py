@@ -141,6 +141,7 @@ class PolicyIndex:
         self._decode = selections_for_bins(grid, gb.sel[self._p], gb.count[self._p])
 
     def select_many(self, caps: Sequence[float]) -> list[Selection]:
+        from . import _native as N
         from .engine import _torch, require_device
 
         caps = [float(c) for c in caps]
@@ -148,6 +149,10 @@ class PolicyIndex:
             _check_cap(c)
         if not caps:
             return []
+        if len(caps) <= 4096:  # latency path: host buffers, one lookup launch
+            # a NaN cap bisects to the end in the reference (policy.py:139)
+            bins = self._tables.query(N.CS_QUERY_BINS, [math.inf if c != c else c for c in caps])
+            return [self._decode[b] for b in bins.tolist()]
         torch = _torch()
         dev = require_device()
         n = len(caps)
@@ -182,13 +187,20 @@ def select_configs(grid: ProfileGrid, kind: PolicyKind, caps: Sequence[float], *
         _check_cap(c)
     if not caps:
         return []
-    torch = _torch()
-    dev = require_device()
     tables = Tables.for_grid(grid, "f64", batching_mtl=batching_mtl, multi_tenant_bs=multi_tenant_bs)
-    sel, cnt = tables.select_caps(0, p, torch.tensor(caps, dtype=torch.float64, device=dev))
+    if len(caps) <= 4096:  # latency path: host buffers, one select launch
+        from . import _native as N
+
+        sel, cnt = tables.query(N.CS_QUERY_SELECT, caps, 0, p)
+        sel, cnt = sel.tolist(), cnt.tolist()
+    else:
+        torch = _torch()
+        dev = require_device()
+        sel, cnt = tables.select_caps(0, p, torch.tensor(caps, dtype=torch.float64, device=dev))
+        sel, cnt = sel.cpu().tolist(), cnt.cpu().tolist()
     cfgs = grid.columns()[0]
     out = []
-    for s, c in zip(sel.cpu().tolist(), cnt.cpu().tolist()):
+    for s, c in zip(sel, cnt):
         if s < 0:
             out.append(IDLE_SELECTION)
         else:
@@ -202,15 +214,14 @@ def feasible_set(grid: ProfileGrid, kind: PolicyKind, cap_w: float, *, batching_
                  multi_tenant_bs: int = 1) -> set[Config]:
     """Configs of the regime whose power fits under the cap (policy.py:151-169); the sampling
     regime searches the combination space. Runs the warp-ballot kernel."""
-    from .engine import Tables, _torch, require_device
+    from .engine import Tables
 
     _check_cap(cap_w)
     p = 2 if kind.tag is PolicyTag.SAMPLING else _POLICY_INDEX[kind.tag]
-    torch = _torch()
-    dev = require_device()
+    from . import _native as N
+
     tables = Tables.for_grid(grid, "f64", batching_mtl=batching_mtl, multi_tenant_bs=multi_tenant_bs)
-    mask = tables.feasible_caps(0, p, torch.tensor([float(cap_w)], dtype=torch.float64, device=dev))
-    words = mask.cpu().numpy().view(np.uint32)[0]
+    words = tables.query(N.CS_QUERY_FEASIBLE, [float(cap_w)], 0, p)[0]
     cfgs = grid.columns()[0]
     out = set()
     for w, bits in enumerate(words.tolist()):
