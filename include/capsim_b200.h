@@ -172,6 +172,7 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* t, const void* caps_host,
 /* ---- online controller replay: controller.replay (controller.py:161-231), one thread per trace ---- */
 #define CS_CTRL_REACTIVE 0
 #define CS_CTRL_PROACTIVE 1
+#define CS_CTRL_TIME_MAJOR 256 /* OR into mode: caps_dev is [n_steps][ld] (ld >= n_traces), coalesced per step */
 typedef struct {
   double measured_power_w; /* power fed to the step (selection's power x seeded noise) */
   uint16_t bin_reactive;   /* grid bin of the selection after the reactive part (0xFFFF: initial config) */

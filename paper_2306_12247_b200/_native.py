@@ -28,6 +28,8 @@ CS_FLAG_CHECK_VIOLATIONS = 1
 CS_FLAG_ACCUMULATE_HIST = 2
 CS_FLAG_SEGMENT_EPILOGUE = 4
 
+CS_CTRL_TIME_MAJOR = 256
+
 CS_QUERY_BINS = 0
 CS_QUERY_SELECT = 1
 CS_QUERY_FEASIBLE = 2

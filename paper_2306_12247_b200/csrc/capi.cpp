@@ -487,7 +487,10 @@ int cs_replay(const cs_tables* tp, int32_t grid, const double* caps_dev, int64_t
   if (d->view.cap_dtype != CS_CAP_F64) return fail(CS_E_INVALID, "cs_replay needs tables staged for fp64 caps");
   if (grid < 0 || grid >= d->view.M) return fail(CS_E_INVALID, "grid out of range");
   if (n_steps < 1 && n_traces > 0) return fail(CS_E_INVALID, "cannot replay an empty trace");
-  if (ld < n_steps || (mode != CS_CTRL_REACTIVE && mode != CS_CTRL_PROACTIVE) || !(noise_pct >= 0.0) || !agg_dev)
+  const int32_t base_mode = mode & 0xFF;
+  const bool tmaj = (mode & CS_CTRL_TIME_MAJOR) != 0;
+  if ((tmaj ? ld < n_traces : ld < n_steps) || (base_mode != CS_CTRL_REACTIVE && base_mode != CS_CTRL_PROACTIVE) ||
+      (mode & ~(0xFF | CS_CTRL_TIME_MAJOR)) || !(noise_pct >= 0.0) || !agg_dev)
     return fail(CS_E_INVALID, "bad replay arguments");
   if (keys_dev && !key_len_dev) return fail(CS_E_INVALID, "keys need key lengths");
   std::string err = cs::launch_replay(d->view, grid, caps_dev, n_traces, n_steps, ld, mode, window_k, initial_dev,

@@ -61,7 +61,11 @@ __global__ void replay_kernel(const DevTables tb, int g, const double* __restric
                               cs_replay_agg* __restrict__ agg) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
-  const double* c = caps + t * ld;
+  // time-major caps ([S][ld], ld >= T): a warp's 32 traces read 256 contiguous bytes per step
+  const bool tm = (mode & CS_CTRL_TIME_MAJOR) != 0;
+  mode &= 0xFF;
+  const double* c = tm ? caps + t : caps + t * ld;
+  const int64_t cstride = tm ? ld : 1;
   Mt rng;
   if (noise_pct > 0.0) {
     uint32_t kbuf[kMaxKey];
@@ -87,14 +91,14 @@ __global__ void replay_kernel(const DevTables tb, int g, const double* __restric
     cur.pw = tb.e_pw[e];
     cur.thr = tb.e_thr[e];
   } else {
-    cur = select_comb(tb, g, c[0]);
+    cur = select_comb(tb, g, c[0]);  // step 0 (same element in both layouts)
   }
   double hist[kMaxWindow];
   int hlen = 0, hpos = 0;
   long long viol = 0, rec = 0;
   double th = 0.0, tl = 0.0;
   for (int64_t i = 0; i < S; ++i) {
-    const double cap = c[i];
+    const double cap = c[i * cstride];
     double meas = cur.entry < 0 ? 0.0 : cur.pw;
     if (noise_pct > 0.0 && cur.entry >= 0) {
       const double r = mt_random(rng);
