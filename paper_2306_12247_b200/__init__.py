@@ -7,8 +7,9 @@ combination policies and simulate(); every decision runs in hand-written sm_100a
 (libcapsim_b200.so via ctypes). Use it as ``import paper_2306_12247_b200 as capsim``.
 
 Also on the GPU: the online controller replay (controller.py) and the
-sampling selector (select_sampling / simulate with sampling_policy, §8(f) rank 2).
-Out of scope: the CLI.
+sampling selector (select_sampling / simulate with sampling_policy, §8(f) rank 2). Trace CSVs
+load through a native parser (load_trace / load_traces / load_trace_matrix, rank 3) and sweeps
+serialise as Parquet tables (columnar.py, rank 4). Out of scope: the CLI.
 """
 
 from .controller import (
