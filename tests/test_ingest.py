@@ -182,3 +182,21 @@ def test_fuzz_native_vs_rules(tmp_path):
             assert got == want and got.start_time == want.start_time
             assert all(math.copysign(1, a) == math.copysign(1, b) for a, b in zip(got.values, want.values))
     assert checked > 60
+
+
+def test_os_errors_match_the_reference_loader(tmp_path):
+    """Unreadable paths fall through to the rules loader, which raises what open() raises."""
+    with pytest.raises(FileNotFoundError):
+        cs.load_trace(tmp_path / "missing.csv", 60)
+    with pytest.raises(IsADirectoryError):
+        cs.load_trace(tmp_path, 60)
+    with pytest.raises(ValueError, match="step_seconds must be positive"):
+        cs.load_traces([tmp_path / "missing.csv"], 0)
+
+
+def test_large_gap_fill_and_long_rows(tmp_path):
+    p = tmp_path / "gappy.csv"
+    p.write_text("timestamp,capacity_w\n2020-01-01T00:00:00Z,5.5\n2021-01-01T00:00:00Z,6.5\n")
+    tr = cs.load_trace(p, 60, gap_fill=True)
+    assert len(tr) == 366 * 1440 + 1 and tr.values[-2] == 5.5 and tr.values[-1] == 6.5
+    assert "_cs_values" in tr.__dict__  # filled natively
