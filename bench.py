@@ -239,21 +239,38 @@ def main() -> None:
 
     # the step's launch sequence (prep, eval[, finalize]) is replayed from a CUDA graph: one graph
     # launch per step instead of the Python/ctypes host path (which dominates C1/C2)
-    graph = None if args.no_graph else tables.capture(caps, S, step_seconds=cfg["step_seconds"],
-                                                        switch_penalty_s=cfg["penalty"], check_violations=True,
-                                                        want_hist=True)
+    ekw = dict(step_seconds=cfg["step_seconds"], switch_penalty_s=cfg["penalty"], check_violations=True,
+               want_hist=True)
+    # two captured graphs with their own output buffers: step k's histogram all-reduce (a side
+    # stream, N > 1) overlaps step k+1's kernels; a buffer is reused only after its reduce is done
+    graphs = [] if args.no_graph else [tables.capture(caps, S, **ekw) for _ in range(2 if world > 1 else 1)]
+    side = torch.cuda.Stream() if world > 1 else None
+    reduced = [None, None]  # event: that buffer's all-reduce finished
+    nstep = [0]
 
     def step():
-        if graph is not None:
-            r = graph.replay()
-        else:
-            r = tables.evaluate(caps, S, step_seconds=cfg["step_seconds"], switch_penalty_s=cfg["penalty"],
-                                check_violations=True, want_hist=True)
-        reduce_histogram(r.hist)  # the single collective: global config histogram (int64, NCCL)
+        k = nstep[0] % max(1, len(graphs))
+        nstep[0] += 1
+        if reduced[k] is not None:
+            stream.wait_event(reduced[k])
+        r = graphs[k].replay() if graphs else tables.evaluate(caps, S, **ekw)
+        if side is None:
+            reduce_histogram(r.hist)  # single rank: a no-op
+            return r
+        done = torch.cuda.Event()
+        done.record(stream)
+        side.wait_event(done)
+        with torch.cuda.stream(side):
+            reduce_histogram(r.hist)  # the single collective: global config histogram (int64, NCCL)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        reduced[k] = ev
         return r
 
     for _ in range(args.warmup):
         res = step()
+    if side is not None:
+        stream.wait_stream(side)
     torch.cuda.synchronize()
     launches_per_step = tables.launch_count()
     if pg is not None:
@@ -266,6 +283,8 @@ def main() -> None:
         for _ in range(args.steps):
             res = step()
             kern_ms.append(None)
+        if side is not None:
+            stream.wait_stream(side)  # the last reduce belongs to the timed region
         ev1.record(stream)
         torch.cuda.synchronize()
     if pg is not None:
@@ -332,7 +351,8 @@ def main() -> None:
                        "grids": M, "policies": 3, "union_bins": tables.n_union_bins,
                        "step_seconds": cfg["step_seconds"], "switch_penalty_s": cfg["penalty"],
                        "trace_kind": cfg["kind"], "parallelism": f"trace-sharded x{world}",
-                       "launch": "cuda-graph replay" if graph is not None else "host path",
+                       "launch": ("cuda-graph replay" + (" x2, reduce overlapped" if side is not None else ""))
+                       if graphs else "host path",
                        "dist_backend": backend if world > 1 else None,
                        "l2": f"inputs {T_total * S * 4 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
                        "policy_evaluations_per_step": T_total * S * M * 3, "plan": plan},
