@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -498,6 +499,8 @@ struct Lut32 {
   }
 };
 
+constexpr uint32_t kStepZero = 0xFFFFFFFFu;  // "no previous step" (never a bin)
+
 // The hot loop over one segment [s0, s1e) of trace t. Returns true if a cap met a LUT leaf
 // that is not proven violation-free (the caller then recounts violations exactly).
 template <bool PEN, bool STEP, bool VIO>
@@ -523,7 +526,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
             atomicAdd(&sw[s_segoff[m * 3 + p] + (int)((s_sig[(size_t)m * U + cb] >> (16 * p)) & 0xFFFFull)], 1u);
       }
   };
-  auto vec4 = [&](const uint4 raw, int v) {
+  // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
+  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4]) {
     const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t e[4];
 #pragma unroll
@@ -534,7 +538,6 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       e[k] = L.entry(u[k]);
 #endif
     }
-    uint32_t b[4];
     const uint32_t any = e[0] | e[1] | e[2] | e[3];
     if ((int32_t)any >= 0) {  // no redirect (marker 0xFFF.....; leaves have bit 31 clear while U < 2^15)
       if (VIO) flags |= any;
@@ -571,59 +574,101 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       atomicAdd(&h[b[k]], 1u);
 #endif
     }
-    const int64_t i0 = s0 + 4 * (int64_t)v;
-    if (PEN) {
-      uint32_t pb = b[0];  // step 0 is never penalised (sim.py:119)
-      if (i0 > 0) {
-        uint32_t dummy = 0;
-        pb = L.bin(__ldg(row + i0 - 1), dummy);
-      }
-      if (M == 1) {  // one signature load per step, chained through the vector
-        uint64_t sg[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sg[k] = s_sig[b[k]];
-        const uint64_t sp = pb == b[0] ? sg[0] : s_sig[pb];
-        auto sw1 = [&](uint64_t sc, uint64_t sprev) {
-          const uint64_t xo = sc ^ sprev;
-          if (xo) {
-#pragma unroll
-            for (int p = 0; p < 3; ++p)
-              if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[so[p] + (int)((sc >> (16 * p)) & 0xFFFFull)], 1u);
-          }
-        };
-        sw1(sg[0], sp);
-        sw1(sg[1], sg[0]);
-        sw1(sg[2], sg[1]);
-        sw1(sg[3], sg[2]);
-      } else {
-        switches(b[0], pb);
-        switches(b[1], b[0]);
-        switches(b[2], b[1]);
-        switches(b[3], b[2]);
-      }
-    }
     if (STEP) {
       uint2 o;
       o.x = (b[0] & 0xFFFFu) | (b[1] << 16);
       o.y = (b[2] & 0xFFFFu) | (b[3] << 16);
-      *reinterpret_cast<uint2*>(P.step_bins + t * P.ld_bins + i0) = o;
+      *reinterpret_cast<uint2*>(P.step_bins + t * P.ld_bins + s0 + 4 * (int64_t)v) = o;
+    }
+  };
+  // switched steps of one vector given pb, the bin of the cap before it (PEN)
+  auto sw4 = [&](const uint32_t (&b)[4], uint32_t pb) {
+    if (M == 1) {  // one signature load per step, chained through the vector
+      uint64_t sg[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sg[k] = s_sig[b[k]];
+      const uint64_t sp = pb == b[0] ? sg[0] : s_sig[pb];
+      auto sw1 = [&](uint64_t sc, uint64_t sprev) {
+        const uint64_t xo = sc ^ sprev;
+        if (xo) {
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+            if ((xo >> (16 * p)) & 0xFFFFull) atomicAdd(&sw[so[p] + (int)((sc >> (16 * p)) & 0xFFFFull)], 1u);
+        }
+      };
+      sw1(sg[0], sp);
+      sw1(sg[1], sg[0]);
+      sw1(sg[2], sg[1]);
+      sw1(sg[3], sg[2]);
+    } else {
+      switches(b[0], pb);
+      switches(b[1], b[0]);
+      switches(b[2], b[1]);
+      switches(b[3], b[2]);
     }
   };
 
-  // rolling software pipeline: each vector's reload is issued as soon as it is consumed, so a
-  // warp keeps 3-4 128-bit loads per lane in flight while it works (not 4, then 0)
-  int v = gtid;
-  for (; v + 3 * gsize < nvf; v += 4 * gsize) {
-    const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
-    const uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
-    const uint4 r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16);
-    const uint4 r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
-    vec4(r0, v);
-    vec4(r1, v + gsize);
-    vec4(r2, v + 2 * gsize);
-    vec4(r3, v + 3 * gsize);
+  if constexpr (PEN) {
+    // Warp-contiguous chunks: each warp owns a run of vectors, lanes interleaved inside it, so the
+    // cap before lane l's vector is lane l-1's last cap (a shuffle) and lane 0's is lane 31's of
+    // the previous pass (carried in a register); only a warp's first vector reloads a cap.
+    const int lane = gtid & 31, nwg = gsize >> 5;
+    const int per = (((nvf + nwg - 1) / nwg) + 7) & ~7;  // 128-B aligned warp chunks
+    const int vb = min(nvf, (gtid >> 5) * per), ve = min(nvf, vb + per);
+    uint32_t carry = 0;
+    if (vb < ve) {
+      const int64_t i0 = s0 + 4 * (int64_t)vb;
+      uint32_t dummy = 0;
+      carry = i0 > 0 ? L.bin(__ldg(row + i0 - 1), dummy) : kStepZero;  // step 0 is never penalised (sim.py:119)
+    }
+    auto pass = [&](const uint4 raw, int v) {
+      uint32_t b[4] = {0u, 0u, 0u, 0u};
+      const bool act = v < ve;
+      if (act) bins4(raw, v, b);
+      const uint32_t left = __shfl_sync(0xffffffffu, b[3], (lane + 31) & 31);
+      uint32_t pb = lane == 0 ? carry : left;
+      carry = __shfl_sync(0xffffffffu, b[3], 31);
+      if (pb == kStepZero) pb = b[0];
+      if (act) sw4(b, pb);
+    };
+    int base = vb;
+    for (; base + 96 < ve; base += 128) {
+      const int v = base + lane;
+      const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
+      const uint4 r1 = ldg_stream(vrow + (size_t)(v + 32) * 16);
+      const uint4 r2 = ldg_stream(vrow + (size_t)(v + 64) * 16);
+      uint4 r3 = make_uint4(0u, 0u, 0u, 0u);
+      if (v + 96 < ve) r3 = ldg_stream(vrow + (size_t)(v + 96) * 16);
+      pass(r0, v);
+      pass(r1, v + 32);
+      pass(r2, v + 64);
+      pass(r3, v + 96);
+    }
+    for (; base < ve; base += 32) {
+      const int v = base + lane;
+      uint4 r = make_uint4(0u, 0u, 0u, 0u);
+      if (v < ve) r = ldg_stream(vrow + (size_t)v * 16);
+      pass(r, v);
+    }
+  } else {
+    auto vec4 = [&](const uint4 raw, int v) {
+      uint32_t b[4];
+      bins4(raw, v, b);
+    };
+    // each lane keeps 4 independent 128-bit loads in flight per pass
+    int v = gtid;
+    for (; v + 3 * gsize < nvf; v += 4 * gsize) {
+      const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
+      const uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
+      const uint4 r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16);
+      const uint4 r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
+      vec4(r0, v);
+      vec4(r1, v + gsize);
+      vec4(r2, v + 2 * gsize);
+      vec4(r3, v + 3 * gsize);
+    }
+    for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
   }
-  for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
   // tail (< 4 caps at the very end of a trace)
   for (int i = 4 * nvf + gtid; i < n; i += gsize) {
     const int64_t gi = s0 + i;
@@ -794,7 +839,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   if (PEN)
     for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
   if (gtid < M * 3) vcnt[gtid] = 0u;
-  if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag
+  if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag (the plan keeps 3M < group size)
   __syncthreads();
 
   Lut64 L64;
@@ -1031,6 +1076,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   const bool small = (double)a->n_traces * (double)a->n_steps < (double)(1 << 22);
   // tiny launches (fewer traces than SMs, <= 1M timesteps): a trace per CTA, all its warps on it
   const bool tiny = a->n_traces < nsm && (double)a->n_traces * (double)a->n_steps <= (double)(1 << 20);
+  static const int force_wpg = std::getenv("CS_PLAN_WPG") ? std::atoi(std::getenv("CS_PLAN_WPG")) : 0;  // tuning only
   auto search = [&](size_t lut_b) {
     Cand b;
     const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;
@@ -1040,6 +1086,8 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
           const int wpc = threads / 32;
           if (wpg > wpc) continue;
           if (tiny ? wpg != wpc : wpg == 32) continue;  // tiny: one whole-CTA group per trace
+          if (force_wpg && wpg != force_wpg) continue;
+          if (wpg * 32 < M * 3 + 1) continue;  // one thread per violation counter (+ the flag)
           const int gpc = wpc / wpg;
           if (wpg > 1 && gpc > 15) continue;  // named barriers 1..15
           size_t o1, o2, o3;
@@ -1058,9 +1106,11 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   };
   Cand c = search(lut_bytes);
   bool big = false;
-  if (f32 && view.n_lut_big > 0 && !small) {
+  if (f32 && view.n_lut_big > 0 && !small && !std::getenv("CS_PLAN_NO_BIG")) {  // env: tuning only
     const Cand cb = search(a16((size_t)view.n_lut_big * 4));
-    if (cb.warps >= c.warps && cb.warps > 0 && (cb.staged || !c.staged)) c = cb, big = true;
+    // ... and no bigger worker groups: a group's barriers and per-trace epilogue cost more than the
+    // finer LUT saves (C5: 8-warp groups with the big LUT 5.41 ms, 4-warp groups with the main 4.99)
+    if (cb.warps >= c.warps && cb.warps > 0 && cb.wpg <= c.wpg && (cb.staged || !c.staged)) c = cb, big = true;
   }
   const size_t lut_b = big ? a16((size_t)view.n_lut_big * 4) : lut_bytes;  // the LUT staged
   const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;

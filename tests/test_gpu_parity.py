@@ -248,6 +248,43 @@ def test_engine_split_trace_and_fine_grid(cs, torch):
     _engine_vs_oracle(cs, torch, [g], _random_caps(rng, 3, 70_000, "iid"), 60, 0.0)
 
 
+@pytest.mark.parametrize("T,S", [(3000, 300), (4100, 1024)])
+def test_fine_grid_multiwarp_groups_many_traces(cs, torch, T, S):
+    """Fine 8x512 grid (2,038 bins -> multi-warp worker groups) with several traces per group, so a
+    group's warp 0 is still writing trace t's records while its other warps run trace t+1; both
+    sizes (plain, and >= 4M timesteps with staged tables) with and without a switching penalty,
+    through the bench's kernel (no per-step output): aggregates vs the oracle, switch counts vs
+    the selections of a per-step run."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(21)
+    g = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
+    caps = _random_caps(rng, T, S, "smooth")
+    ld = (S + 3) // 4 * 4
+    host = np.zeros((T, ld), np.float32)
+    host[:, :S] = caps
+    dev = torch.from_numpy(host).cuda()
+    t = cs.Tables.stage([g], "f32")
+    gb = t.grid_bins(0)
+    for pen in (0.0, 10.0):
+        res = t.evaluate(dev, S, step_seconds=60, switch_penalty_s=pen)
+        plan = t.last_plan()
+        assert plan["warps_per_group"] > 1 and T > 2 * plan["ctas"] * plan["threads"] // 32 // plan["warps_per_group"]
+        avg, idle, en, _ = oracle.simulate_batch([oracle_grid(g)], caps, 60, pen, n_threads=8)
+        assert np.array_equal(res.idle_steps.cpu().numpy(), idle)
+        assert np.all(res.violations.cpu().numpy() == 0)
+        g_avg, g_en = res.avg_throughput_ips.cpu().numpy(), res.energy_proxy_wh.cpu().numpy()
+        assert np.allclose(g_avg, avg, rtol=REL_TOL, atol=0) and np.allclose(g_en, en, rtol=REL_TOL, atol=0)
+        assert np.mean(g_avg == avg) > 0.999
+        ps = t.evaluate(dev, S, step_seconds=60, switch_penalty_s=pen, per_step=True)
+        ub = ps.step_bins[:, :S].cpu().numpy().view(np.uint16).astype(np.int64)
+        assert np.array_equal(res.hist.cpu().numpy(), np.bincount(ub.ravel(), minlength=t.n_union_bins))
+        for p in range(3):
+            sel = gb.sel[p][gb.umap[ub]]
+            want = np.sum(sel[:, 1:] != sel[:, :-1], axis=1) if pen > 0 else np.zeros(T, np.int64)
+            assert np.array_equal(res.switches[:, 0, p].cpu().numpy().astype(np.int64), want), p
+
+
 def test_engine_random_and_tie_grids(cs, torch):
     doc = golden("policy_golden.json")
     rng = np.random.default_rng(14)

@@ -24,6 +24,13 @@ t32.evaluate(big, 300000, step_seconds=60, switch_penalty_s=10.0)  # split trace
 t1 = cs.Tables.stage([g], "f32")
 many = cs.generate_traces(420, 10080, step_seconds=60, kind="mixed", seed=5)
 t1.evaluate(many, 10080, step_seconds=60)  # big LUT + per-bin epilogue
+# fine grid (2,038 bins): multi-warp worker groups, several traces each (warp 0 finishes a trace's
+# records while the group's other warps start the next)
+fine = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0, model_name="fine"))
+tf = cs.Tables.stage([fine], "f32")
+fc = cs.generate_traces(4000, 256, step_seconds=60, kind="mixed", seed=6)
+tf.evaluate(fc, 256, step_seconds=60, switch_penalty_s=10.0)
+tf.evaluate(fc, 256, step_seconds=60)
 t64 = cs.Tables.stage([g], "f64")
 t64.evaluate(caps.double(), 2000, step_seconds=60, switch_penalty_s=5.0)
 idx = cs.PolicyIndex(g, cs.COMBINATION)
