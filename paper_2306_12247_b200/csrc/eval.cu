@@ -358,11 +358,11 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
       const int kidle = sidle[mp] ? k0 : -1;         // the idle selection is always the first segment
       double a[4] = {0.0, 0.0, 0.0, 0.0};  // thr hi, lo, energy hi, lo
       uint32_t idle = 0, swc = 0;
-      for (int k = k0 + gtid; k < k1; k += gsize) {
+      auto seg = [&](int k) {
         const uint32_t hd = shdr[k];
         const uint32_t ulo = hd & 0xFFFFu, uhi = hd >> 16;
         const uint32_t cnt = C[uhi] - (ulo ? C[ulo - 1] : 0u);
-        if (cnt == 0) continue;
+        if (cnt == 0) return;
         const double dc = (double)cnt;
         const double2 ve = sval[NS + k];
         a[2] = __fma_rn(dc, ve.x, a[2]);
@@ -386,7 +386,15 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
             a[1] = __fma_rn(ds, vp.y, a[1]);
           }
         }
+      };
+      // two segments per iteration so their dependent load chains (header -> prefix counts ->
+      // values) overlap; same accumulation order as one at a time
+      int k = k0 + gtid;
+      for (; k + gsize < k1; k += 2 * gsize) {
+        seg(k);
+        seg(k + gsize);
       }
+      if (k < k1) seg(k);
       mine[p] = xreduce4(a, lane);
       ired[p] = __reduce_add_sync(0xffffffffu, idle);
       ired[3 + p] = PEN ? __reduce_add_sync(0xffffffffu, swc) : 0u;
