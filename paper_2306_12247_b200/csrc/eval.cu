@@ -97,6 +97,11 @@ struct EvalParams {
   const uint32_t* seg_hdr;
   const int32_t* seg_idle;
   const double* seg_val;
+  // compact form for the epilogue that reads them from global memory: per segment the unsplit
+  // {thr (0 when idle), energy} pair; per (grid, policy) {Q_thr, 1/Q_thr, Q_energy, 1/Q_energy}
+  // (the split is recomputed with the same formula: split_q)
+  const double2* seg_raw;
+  const double* seg_q;
   int32_t off_seg, seg_smem_bytes;
   // bin epilogue (one grid, no penalty): per union bin u and policy p the {hi, lo} pairs of the
   // step's throughput and energy, bin_val[(2p + j) * U4 + u] (j = 0 thr, 1 energy), staged at
@@ -150,13 +155,15 @@ __device__ __forceinline__ void count_switches(uint64_t sc, uint64_t sprev, int 
 // hi + lo rounds to the exactly rounded sum the reference's math.fsum returns.
 // Segment tables (structure of arrays, one block per (grid, policy)): seg_hdr[k] = u_lo | u_hi << 16,
 // {hi, lo} pairs seg_val2[j * NSEG + k] for j = thr, energy, penalised thr, and seg_idle[mp].
-__device__ __forceinline__ double2 split2(double v, int eq) {
-  const double hi = ldexp(floor(ldexp(v, -eq)), eq);  // floor(v / Q) * Q, exact
-  return make_double2(hi, v - hi);
+__device__ __forceinline__ double2 split_q(double v, double q, double qi) {
+  const double hi = __dmul_rn(floor(__dmul_rn(v, qi)), q);  // floor(v / Q) * Q, exact (powers of two)
+  return make_double2(hi, __dsub_rn(v, hi));
 }
+__device__ __forceinline__ double quantum(int eq) { return ldexp(1.0, max(-1000, min(1000, eq))); }
 
 __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, int nseg, uint32_t* hdr,
-                            int32_t* idlef, double* val, double2* binval, int U4) {  // L: see split2
+                            int32_t* idlef, double* val, double2* binval, int U4, double2* raw,
+                            double* qtab) {  // L: see split_q
   __shared__ double red[2][256];
   const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
   const size_t ob = (size_t)mp * B;
@@ -182,13 +189,15 @@ __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, 
   frexp(red[1][0] > 0.0 ? red[1][0] : 1.0, &ee);
   et -= L;
   ee -= L;
+  const double qt = quantum(et), qit = quantum(-et), qe = quantum(ee), qie = quantum(-ee);
+  if (threadIdx.x == 0) qtab[4 * mp] = qt, qtab[4 * mp + 1] = qit, qtab[4 * mp + 2] = qe, qtab[4 * mp + 3] = qie;
   if (binval) {  // bin epilogue tables (M == 1: union bins are the grid's bins)
     const int p = mp % 3;
     for (int r = threadIdx.x; r < B; r += blockDim.x) {
       const bool idle = tb.sel[ob + r] < 0;
-      binval[(size_t)(2 * p) * U4 + r] = split2(idle ? 0.0 : tb.sthr[ob + r], et);
+      binval[(size_t)(2 * p) * U4 + r] = split_q(idle ? 0.0 : tb.sthr[ob + r], qt, qit);
       binval[(size_t)(2 * p + 1) * U4 + r] =
-          split2(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[ob + r], step), 3600.0), ee);
+          split_q(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[ob + r], step), 3600.0), qe, qie);
     }
   }
   const int k0 = tb.seg_off[mp], k1 = tb.seg_off[mp + 1];
@@ -198,9 +207,12 @@ __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, 
     const size_t i = ob + sg.z;
     const bool idle = tb.sel[i] < 0;  // only ever the first segment (feasibility is monotone in the cap)
     hdr[k] = (uint32_t)sg.x | ((uint32_t)sg.y << 16);
-    const double2 t = split2(idle ? 0.0 : tb.sthr[i], et);
-    const double2 e = split2(idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0), ee);
-    const double2 q = split2(idle ? 0.0 : __dmul_rn(tb.sthr[i], omp), et);
+    const double thr = idle ? 0.0 : tb.sthr[i];
+    const double en = idle ? idle_e : __ddiv_rn(__dmul_rn(tb.spw[i], step), 3600.0);
+    raw[k] = make_double2(thr, en);
+    const double2 t = split_q(thr, qt, qit);
+    const double2 e = split_q(en, qe, qie);
+    const double2 q = split_q(__dmul_rn(thr, omp), qt, qit);  // idle: 0 * omp = 0
     double2* v2 = reinterpret_cast<double2*>(val);
     v2[0 * (size_t)nseg + k] = t;
     v2[1 * (size_t)nseg + k] = e;
@@ -338,7 +350,7 @@ __device__ __forceinline__ void store_aggs(const EvalParams& P, int64_t t, int m
 // then one transposed warp reduction per policy; lanes 0..2 finalize one policy each.
 //   C[u]                prefix-summed step counts (scanned in place)
 //   SW[(m*3+p)*U4 + u]  prefix-summed switched-step counts (PEN)
-template <bool PEN>
+template <bool PEN, bool COMPACT>
 __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
                                          const uint32_t* vcnt, const uint32_t* shdr, const int32_t* sidle,
                                          const double2* sval, double* scratch, int gtid, int gsize, int gid_local,
@@ -358,13 +370,18 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
       const int kidle = sidle[mp] ? k0 : -1;         // the idle selection is always the first segment
       double a[4] = {0.0, 0.0, 0.0, 0.0};  // thr hi, lo, energy hi, lo
       uint32_t idle = 0, swc = 0;
+      double qt = 0.0, qit = 0.0, qe = 0.0, qie = 0.0;
+      if (COMPACT) qt = __ldg(P.seg_q + 4 * mp), qit = __ldg(P.seg_q + 4 * mp + 1), qe = __ldg(P.seg_q + 4 * mp + 2),
+                   qie = __ldg(P.seg_q + 4 * mp + 3);
       auto seg = [&](int k) {
         const uint32_t hd = shdr[k];
         const uint32_t ulo = hd & 0xFFFFu, uhi = hd >> 16;
         const uint32_t cnt = C[uhi] - (ulo ? C[ulo - 1] : 0u);
         if (cnt == 0) return;
         const double dc = (double)cnt;
-        const double2 ve = sval[NS + k];
+        double2 r = make_double2(0.0, 0.0);
+        if (COMPACT) r = __ldg(P.seg_raw + k);  // 16 B instead of 48 B of pre-split values
+        const double2 ve = COMPACT ? split_q(r.y, qe, qie) : sval[NS + k];
         a[2] = __fma_rn(dc, ve.x, a[2]);
         a[3] = __fma_rn(dc, ve.y, a[3]);
         uint32_t scnt = 0;
@@ -376,12 +393,12 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
           idle += cnt;  // idle segments carry zero throughput
         } else {
           const double dn = (double)(cnt - scnt);
-          const double2 vt = sval[k];
+          const double2 vt = COMPACT ? split_q(r.x, qt, qit) : sval[k];
           a[0] = __fma_rn(dn, vt.x, a[0]);
           a[1] = __fma_rn(dn, vt.y, a[1]);
           if (PEN && scnt) {
             const double ds = (double)scnt;
-            const double2 vp = sval[2 * NS + k];
+            const double2 vp = COMPACT ? split_q(__dmul_rn(r.x, P.omp), qt, qit) : sval[2 * NS + k];
             a[0] = __fma_rn(ds, vp.x, a[0]);
             a[1] = __fma_rn(ds, vp.y, a[1]);
           }
@@ -446,7 +463,7 @@ __device__ __forceinline__ void finish_trace_bins(const EvalParams& P, int64_t t
 
 // Scan + epilogue over a group histogram (smem in the main kernel, global in finalize); the
 // histogram (and switch histograms) are left zeroed for the next trace.
-template <bool PEN, typename GH>
+template <bool PEN, bool COMPACT, typename GH>
 __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* sw,
                                              const uint32_t* vcnt, GH* ghist, const uint32_t* shdr,
                                              const int32_t* sidle, const double2* sval, double* scratch, int gtid,
@@ -455,7 +472,7 @@ __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uin
   uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then partial sums
   group_scan(h, U4, ghist, wtot, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
-  epilogue<PEN>(P, t, h, sw, vcnt, shdr, sidle, sval, scratch, gtid, gsize, gid_local);
+  epilogue<PEN, COMPACT>(P, t, h, sw, vcnt, shdr, sidle, sval, scratch, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
   for (int u = 4 * gtid; u < U4; u += 4 * gsize) *reinterpret_cast<uint4*>(h + u) = make_uint4(0u, 0u, 0u, 0u);
   if (PEN)
@@ -916,9 +933,9 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
       if (!PEN && P.bin_epi)
         finish_trace_bins(P, t, h, vcnt, gh, s_binval, scratch, gtid, gsize, gid_local);
       else if (seg_staged)  // two instantiations so each reads its tables with a known address space
-        finish_trace<PEN>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
+        finish_trace<PEN, false>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
       else
-        finish_trace<PEN>(P, t, h, sw, vcnt, gh, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val),
+        finish_trace<PEN, true>(P, t, h, sw, vcnt, gh, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val),
                           scratch, gtid, gsize, gid_local);
     } else {
       // split trace: fold this segment's partial histogram into the trace's global partials
@@ -978,7 +995,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const __grid_constant__ 
   group_sync(0, blockDim.x);
   const uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
   const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
-  epilogue<PEN>(P, t, h, sw, vc, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val), scratch,
+  epilogue<PEN, true>(P, t, h, sw, vc, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val), scratch,
                 threadIdx.x, blockDim.x, 0, split ? m : 0, split ? m + 1 : M);
 }
 
@@ -1069,7 +1086,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   // segment tables (prep_kernel): hdr [NS] u32, idle flags [M*3] i32, values [6][NS] f64 in the
   // workspace; the kernel stages hdr, flags and the 4 (6 with a penalty) value arrays it reads
   const size_t seg_hdr_b = (size_t)((nsegs + 3) & ~3) * 4, seg_idle_b = (size_t)((M * 3 + 3) & ~3) * 4;
-  const size_t seg_ws = a16(seg_hdr_b + seg_idle_b + (size_t)6 * nsegs * 8);
+  const size_t seg_ws = a16(seg_hdr_b + seg_idle_b + (size_t)(6 + 2) * nsegs * 8 + (size_t)M * 3 * 4 * 8);
   // one grid without a penalty: the bin epilogue's per-bin tables replace the segment tables
   const bool bin_epi = !pen && M == 1 && (double)a->n_traces * (double)a->n_steps >= (double)(1 << 22) &&
                        !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
@@ -1238,6 +1255,8 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
     P.seg_hdr = reinterpret_cast<const uint32_t*>(ws);
     P.seg_idle = reinterpret_cast<const int32_t*>(ws + (size_t)((NS + 3) & ~3) * 4);
     P.seg_val = reinterpret_cast<const double*>(ws + (size_t)((NS + 3) & ~3) * 4 + (size_t)((M * 3 + 3) & ~3) * 4);
+    P.seg_raw = reinterpret_cast<const double2*>(P.seg_val + (size_t)6 * NS);
+    P.seg_q = reinterpret_cast<const double*>(P.seg_raw + NS);
   }
   // bits of the exact hi part: counts up to S must keep sum(count x hi) below 2^53 quanta
   int L = 52;
@@ -1247,7 +1266,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, P.NSEG,
                                                     const_cast<uint32_t*>(P.seg_hdr), const_cast<int32_t*>(P.seg_idle),
                                                     const_cast<double*>(P.seg_val), const_cast<double2*>(P.bin_val),
-                                                    P.U4);
+                                                    P.U4, const_cast<double2*>(P.seg_raw), const_cast<double*>(P.seg_q));
   CS_CUDA_TRY(cudaGetLastError());
   ++launches;
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
