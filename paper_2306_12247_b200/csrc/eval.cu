@@ -511,6 +511,7 @@ struct Lut32 {
   const uint32_t* lut;  // shared
   int32_t kb, nbm1;
   uint32_t s1, sub0, mask1;
+  uint32_t s2, mask2;  // shift and leaf mask one level down (s1 - 4)
 
   // level-1 entry: the bucket index is clamped into [0, NB-1]; buckets 0 and NB-1 are empty
   // guards, so -0.0 / negatives land in bin 0 and caps above every threshold in the top bin
@@ -586,27 +587,30 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
     } else {  // redirects (or, for >= 2^15 bins, high bases)
-      // one predicated sub-table step per element, then deep() only for chains (rare)
-      uint32_t sh[4];
+      // one predicated sub-table step per element — a level-1 redirect always splits its bucket
+      // at shift s1 - 4 (staging.cpp: LutBuilder::make), so shift and leaf mask are constants —
+      // then the general loop only for chains (rare)
+      uint32_t msk[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        sh[k] = L.s1;
+        msk[k] = L.mask1;
         if (e[k] >= kRedirect32) {
-          sh[k] = e[k] & 31u;
-          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
+          msk[k] = L.mask2;
+          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> L.s2) & 15u)];
         }
       }
       if (e[0] >= kRedirect32 || e[1] >= kRedirect32 || e[2] >= kRedirect32 || e[3] >= kRedirect32) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           while (e[k] >= kRedirect32) {
-            sh[k] = e[k] & 31u;
-            e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh[k]) & 15u)];
+            const uint32_t sh = e[k] & 31u;
+            e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh) & 15u)];
+            msk[k] = ((1u << sh) - 1u) & 0x3FFFu;
           }
       }
       if (VIO) flags |= e[0] | e[1] | e[2] | e[3];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], ((1u << sh[k]) - 1u) & 0x3FFFu);
+      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], msk[k]);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -895,6 +899,8 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   L.s1 = P.lv.shift1;
   L.sub0 = P.lv.sub0;
   L.mask1 = ((1u << P.lv.shift1) - 1u) & 0x3FFFu;
+  L.s2 = P.lv.shift1 >= 4 ? P.lv.shift1 - 4 : 0;
+  L.mask2 = ((1u << L.s2) - 1u) & 0x3FFFu;
 
   const int64_t n_items = P.T * (int64_t)P.nseg;
   const int64_t n_groups = (int64_t)gridDim.x * P.gpc;
