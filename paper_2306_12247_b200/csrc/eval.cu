@@ -779,11 +779,11 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const Lut64
   };
   // 4 caps (two 128-bit loads) per lane and pass: entries first, then the leaves, for ILP
   const int nq = n >> 2;
-  for (int q = gtid; q < nq; q += gsize) {
+  auto bins4 = [&](int q, uint32_t (&b)[4]) {
     const uint4 ra = ldg_stream(vrow + (size_t)q * 32), rb = ldg_stream(vrow + (size_t)q * 32 + 16);
     uint64_t u[4] = {((uint64_t)ra.y << 32) | ra.x, ((uint64_t)ra.w << 32) | ra.z, ((uint64_t)rb.y << 32) | rb.x,
                      ((uint64_t)rb.w << 32) | rb.z};
-    uint32_t e[4], b[4];
+    uint32_t e[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) u[k] = L.clampu(u[k]);
 #pragma unroll
@@ -792,23 +792,44 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const Lut64
     for (int k = 0; k < 4; ++k) b[k] = L.resolve(e[k], u[k], flags);
 #pragma unroll
     for (int k = 0; k < 4; ++k) atomicAdd(&h[b[k]], 1u);
-    const int64_t gi = s0 + 4 * (int64_t)q;
-    if (PEN) {
-      uint32_t pb = b[0];  // step 0 is never penalised (sim.py:119)
-      if (gi > 0) {
-        uint32_t dummy = 0;
-        pb = L.bin(__ldg(row + gi - 1), dummy);
-      }
-      switches(b[0], pb);
-      switches(b[1], b[0]);
-      switches(b[2], b[1]);
-      switches(b[3], b[2]);
-    }
     if (STEP) {
       uint2 o;
       o.x = (b[0] & 0xFFFFu) | (b[1] << 16);
       o.y = (b[2] & 0xFFFFu) | (b[3] << 16);
-      *reinterpret_cast<uint2*>(P.step_bins + t * P.ld_bins + gi) = o;
+      *reinterpret_cast<uint2*>(P.step_bins + t * P.ld_bins + s0 + 4 * (int64_t)q) = o;
+    }
+  };
+  if constexpr (PEN) {
+    // warp-contiguous runs of 4-cap groups, the previous step's bin through shuffles (as in the
+    // fp32 loop): only a warp's first group reloads a cap
+    const int lane = gtid & 31, nwg = gsize >> 5;
+    const int per = (((nq + nwg - 1) / nwg) + 3) & ~3;  // 128-B aligned warp runs
+    const int qb = min(nq, (gtid >> 5) * per), qe = min(nq, qb + per);
+    uint32_t carry = kStepZero;
+    if (qb < qe && s0 + 4 * (int64_t)qb > 0) {
+      uint32_t dummy = 0;
+      carry = L.bin(__ldg(row + s0 + 4 * (int64_t)qb - 1), dummy);
+    }
+    for (int base = qb; base < qe; base += 32) {
+      const int q = base + lane;
+      const bool act = q < qe;
+      uint32_t b[4] = {0u, 0u, 0u, 0u};
+      if (act) bins4(q, b);
+      const uint32_t left = __shfl_sync(0xffffffffu, b[3], (lane + 31) & 31);
+      uint32_t pb = lane == 0 ? carry : left;
+      carry = __shfl_sync(0xffffffffu, b[3], 31);
+      if (pb == kStepZero) pb = b[0];  // step 0 is never penalised (sim.py:119)
+      if (act) {
+        switches(b[0], pb);
+        switches(b[1], b[0]);
+        switches(b[2], b[1]);
+        switches(b[3], b[2]);
+      }
+    }
+  } else {
+    for (int q = gtid; q < nq; q += gsize) {
+      uint32_t b[4];
+      bins4(q, b);
     }
   }
   for (int i = 4 * nq + gtid; i < n; i += gsize) {  // tail (< 4 caps at the end of the segment)

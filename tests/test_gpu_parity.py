@@ -285,6 +285,30 @@ def test_fine_grid_multiwarp_groups_many_traces(cs, torch, T, S):
             assert np.array_equal(res.switches[:, 0, p].cpu().numpy().astype(np.int64), want), p
 
 
+def test_fp64_penalty_path_matches_fp32(cs, torch):
+    """fp64 caps (the drop-in PowerTrace path) through the penalty loop with multi-warp worker
+    groups (fine grid): on f32-representable caps every selection equals the fp32 path's, so
+    idle and switch counts are identical and the exact sums agree."""
+    rng = np.random.default_rng(22)
+    g = cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
+    T, S = 1500, 2000
+    caps = _random_caps(rng, T, S, "smooth")
+    dev32 = torch.from_numpy(caps).cuda()
+    t32, t64 = cs.Tables.stage([g], "f32"), cs.Tables.stage([g], "f64")
+    for pen in (10.0, 0.0):
+        r32 = t32.evaluate(dev32, S, step_seconds=60, switch_penalty_s=pen)
+        r64 = t64.evaluate(dev32.double(), S, step_seconds=60, switch_penalty_s=pen)
+        assert t64.last_plan()["warps_per_group"] > 1
+        assert torch.equal(r32.switches.cpu(), r64.switches.cpu())
+        assert torch.equal(r32.idle_steps.cpu(), r64.idle_steps.cpu())
+        assert int(r64.violations.sum()) == 0
+        for a, b in ((r32.avg_throughput_ips, r64.avg_throughput_ips), (r32.energy_proxy_wh, r64.energy_proxy_wh)):
+            a, b = a.cpu().numpy(), b.cpu().numpy()
+            assert np.allclose(a, b, rtol=1e-12, atol=0)
+        if pen > 0:
+            assert int(r64.switches.sum()) > T
+
+
 def test_engine_random_and_tie_grids(cs, torch):
     doc = golden("policy_golden.json")
     rng = np.random.default_rng(14)

@@ -1,4 +1,5 @@
-"""fp64 (drop-in PowerTrace values) evaluation throughput: the f32 bench workload widened to fp64."""
+"""fp64 (drop-in PowerTrace values) evaluation throughput: the f32 bench workload widened to fp64.
+Usage: python tools/diag_f64.py [traces] [switch_penalty_s]"""
 import statistics
 import sys
 from pathlib import Path
@@ -12,6 +13,7 @@ import paper_2306_12247_b200 as cs  # noqa: E402
 from paper_2306_12247_b200 import _native as N  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
+PEN = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0  # switching penalty (s)
 S = 10080
 g = cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128))
 caps32 = cs.generate_traces(T, S, step_seconds=60, kind="mixed", seed=2306)
@@ -20,11 +22,11 @@ del caps32
 tab = cs.Tables.stage([g], "f64")
 ms = []
 for i in range(6):
-    tab.evaluate(caps, S, step_seconds=60)
+    tab.evaluate(caps, S, step_seconds=60, switch_penalty_s=PEN)
     torch.cuda.synchronize()
     x = C.c_float()
     N.check(N.lib().cs_eval_last_kernel_ms(C.byref(x)))
     if i >= 2:
         ms.append(x.value)
 m = statistics.median(ms)
-print(f"f64 T={T}: kernel {m:.3f} ms  {T * S / m / 1e9:.3f} Tsteps/s  {T * S * 8 / m / 1e6:.0f} GB/s plan {tab.last_plan()}")
+print(f"f64 T={T} pen={PEN}: kernel {m:.3f} ms  {T * S / m / 1e9:.3f} Tsteps/s  {T * S * 8 / m / 1e6:.0f} GB/s plan {tab.last_plan()}")

@@ -31,6 +31,7 @@ tf = cs.Tables.stage([fine], "f32")
 fc = cs.generate_traces(4000, 256, step_seconds=60, kind="mixed", seed=6)
 tf.evaluate(fc, 256, step_seconds=60, switch_penalty_s=10.0)
 tf.evaluate(fc, 256, step_seconds=60)
+cs.Tables.stage([fine], "f64").evaluate(fc[:600].double(), 256, step_seconds=60, switch_penalty_s=10.0)
 t64 = cs.Tables.stage([g], "f64")
 t64.evaluate(caps.double(), 2000, step_seconds=60, switch_penalty_s=5.0)
 idx = cs.PolicyIndex(g, cs.COMBINATION)
