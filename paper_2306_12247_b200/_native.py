@@ -27,6 +27,7 @@ CS_CAP_F64 = 1
 CS_FLAG_CHECK_VIOLATIONS = 1
 CS_FLAG_ACCUMULATE_HIST = 2
 CS_FLAG_SEGMENT_EPILOGUE = 4
+CS_FLAG_PREPARED = 8
 
 CS_CTRL_TIME_MAJOR = 256
 

@@ -1298,12 +1298,14 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
   int launches = 0;
   P.bin_val = P.bin_epi ? reinterpret_cast<const double2*>(ws + pl.ws_prep - bin_bytes_of(P)) : nullptr;
-  prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, P.NSEG,
-                                                    const_cast<uint32_t*>(P.seg_hdr), const_cast<int32_t*>(P.seg_idle),
-                                                    const_cast<double*>(P.seg_val), const_cast<double2*>(P.bin_val),
-                                                    P.U4, const_cast<double2*>(P.seg_raw), const_cast<double*>(P.seg_q));
-  CS_CUDA_TRY(cudaGetLastError());
-  ++launches;
+  if (!(a->flags & CS_FLAG_PREPARED)) {  // the launch's value tables (constant across graph replays)
+    prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, P.NSEG,
+                                                      const_cast<uint32_t*>(P.seg_hdr), const_cast<int32_t*>(P.seg_idle),
+                                                      const_cast<double*>(P.seg_val), const_cast<double2*>(P.bin_val),
+                                                      P.U4, const_cast<double2*>(P.seg_raw), const_cast<double*>(P.seg_q));
+    CS_CUDA_TRY(cudaGetLastError());
+    ++launches;
+  }
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
   if (pl.nseg > 1) {
     uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);

@@ -149,7 +149,8 @@ class Tables:
     # ---- evaluation ----
     def evaluate(self, caps, n_steps: int | None = None, *, step_seconds: int, switch_penalty_s: float = 0.0,
                  per_step: bool = False, check_violations: bool = True, want_hist: bool = True,
-                 accumulate_hist=None, stream=None, segment_epilogue: bool = False) -> "EvalResult":
+                 accumulate_hist=None, stream=None, segment_epilogue: bool = False,
+                 _prepared_ws=None) -> "EvalResult":
         """N2+N3 over a device cap matrix ``caps`` [T, ld] (torch, cuda, dtype of the tables).
 
         Every (trace, grid, policy) aggregate of simulate() is produced in one pass; per-step
@@ -183,7 +184,8 @@ class Tables:
             a.switch_penalty_s = float(switch_penalty_s)
             a.flags = (N.CS_FLAG_CHECK_VIOLATIONS if check_violations else 0) | (
                 N.CS_FLAG_ACCUMULATE_HIST if accumulate_hist is not None else 0) | (
-                N.CS_FLAG_SEGMENT_EPILOGUE if segment_epilogue else 0)
+                N.CS_FLAG_SEGMENT_EPILOGUE if segment_epilogue else 0) | (
+                N.CS_FLAG_PREPARED if _prepared_ws is not None else 0)
             a.step_bins = bins.data_ptr() if bins is not None else None
             a.ld_bins = ld_bins
             a.agg = agg.data_ptr()
@@ -199,7 +201,13 @@ class Tables:
                                               segment_epilogue=segment_epilogue)
             N.check(rc)
             ws = None
-            if ws_bytes.value:
+            if _prepared_ws is not None:  # EvalGraph: the value tables of an identical earlier launch
+                if _prepared_ws.numel() != ws_bytes.value:
+                    raise ValueError("prepared workspace does not match this launch")
+                ws = _prepared_ws
+                a.workspace = ws.data_ptr()
+                a.workspace_bytes = ws_bytes.value
+            elif ws_bytes.value:
                 ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
                 a.workspace = ws.data_ptr()
                 a.workspace_bytes = ws_bytes.value
@@ -390,19 +398,22 @@ class Tables:
 
 class EvalGraph:
     """One ``Tables.evaluate`` captured as a CUDA graph. ``replay()`` re-runs the launch sequence
-    (prep, eval, finalize kernels and the histogram memset) on the same device buffers in a single
+    (eval, finalize kernels and the histogram memset) on the same device buffers in a single
     graph launch: for latency-bound sweeps (a few traces) the host path — Python, ctypes, plan —
-    costs more than the kernels. Inputs are read from ``caps`` at replay time, so refill it in
-    place to evaluate new data; ``result`` holds the outputs of the latest replay."""
+    costs more than the kernels. The per-launch value tables (prep kernel) depend only on the
+    tables and the arguments, so the warm-up launch writes them once into a workspace the graph
+    keeps (CS_FLAG_PREPARED). Inputs are read from ``caps`` at replay time, so refill it in place
+    to evaluate new data; ``result`` holds the outputs of the latest replay."""
 
     def __init__(self, tables: "Tables", caps, n_steps: int | None = None, **kw):
         torch = _torch()
         self.tables = tables
-        tables.evaluate(caps, n_steps, **kw)  # warm-up outside capture: upload, plan memo, events
+        warm = tables.evaluate(caps, n_steps, **kw)  # outside capture: upload, plan memo, value tables
         torch.cuda.synchronize()
+        self._ws = warm._ws
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
-            self.result = tables.evaluate(caps, n_steps, **kw)
+            self.result = tables.evaluate(caps, n_steps, _prepared_ws=self._ws, **kw)
         torch.cuda.synchronize()
 
     def replay(self) -> "EvalResult":
