@@ -556,9 +556,6 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
                                                 const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
                                                 int gsize) {
   const int U = P.tb.U, M = P.tb.M;
-  const int32_t* s_segoff = reinterpret_cast<const int32_t*>(s_sig + (size_t)M * U);
-  int so[3] = {0, 0, 0};
-  if (PEN) so[0] = s_segoff[0], so[1] = s_segoff[1], so[2] = s_segoff[2];
   const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
@@ -569,8 +566,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
   auto switches = [&](uint32_t cb, uint32_t pb) {
     if (cb != pb)
       for (int m = 0; m < M; ++m)
-        count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], s_segoff[m * 3], s_segoff[m * 3 + 1],
-                       s_segoff[m * 3 + 2], sw_s, sw_dummy);
+        count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], 0, 0, 0, sw_s, sw_dummy);
   };
   // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
   auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4]) {
@@ -637,7 +633,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
 #pragma unroll
       for (int k = 0; k < 4; ++k) sg[k] = s_sig[b[k]];
       const uint64_t sp = pb == b[0] ? sg[0] : s_sig[pb];
-      auto sw1 = [&](uint64_t sc, uint64_t sprev) { count_switches(sc, sprev, so[0], so[1], so[2], sw_s, sw_dummy); };
+      auto sw1 = [&](uint64_t sc, uint64_t sprev) { count_switches(sc, sprev, 0, 0, 0, sw_s, sw_dummy); };
       sw1(sg[0], sp);
       sw1(sg[1], sg[0]);
       sw1(sg[2], sg[1]);
@@ -764,7 +760,6 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const Lut64
                                                 int gsize) {
   const DevTables& tb = P.tb;
   const int U = tb.U, M = tb.M;
-  const int32_t* s_segoff = reinterpret_cast<const int32_t*>(s_sig + (size_t)M * U);
   const unsigned long long* row = reinterpret_cast<const unsigned long long*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
   const int n = (int)(s1e - s0);
@@ -774,8 +769,7 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const Lut64
   auto switches = [&](uint32_t cb, uint32_t pb) {
     if (cb != pb)
       for (int m = 0; m < M; ++m)
-        count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], s_segoff[m * 3], s_segoff[m * 3 + 1],
-                       s_segoff[m * 3 + 2], sw_s, sw_dummy);
+        count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], 0, 0, 0, sw_s, sw_dummy);
   };
   // 4 caps (two 128-bit loads) per lane and pass: entries first, then the leaves, for ILP
   const int nq = n >> 2;
@@ -860,10 +854,16 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   if (!F32)
     for (int i = threadIdx.x; i < U - 1; i += blockDim.x) s_thr[i] = __ldg(P.lv.thr64 + i);
   uint64_t* s_sig = reinterpret_cast<uint64_t*>(smem + P.off_sig);
-  int32_t* s_segoff = reinterpret_cast<int32_t*>(s_sig + (size_t)M * U);  // [M*3+1] (PEN)
   if (PEN) {
-    for (int i = threadIdx.x; i < M * U; i += blockDim.x) s_sig[i] = __ldg(tb.sig + i);
-    for (int i = threadIdx.x; i <= M * 3; i += blockDim.x) s_segoff[i] = __ldg(tb.seg_off + i);
+    // signatures with each (grid, policy)'s first segment index folded in, so the 16-bit fields
+    // are absolute switch-counter indices (the plan keeps NSEG <= 0xFFFF, so no field carries)
+    for (int i = threadIdx.x; i < M * U; i += blockDim.x) {
+      const int m = i / U;
+      const uint64_t fold = (uint64_t)(uint32_t)__ldg(tb.seg_off + 3 * m) |
+                            ((uint64_t)(uint32_t)__ldg(tb.seg_off + 3 * m + 1) << 16) |
+                            ((uint64_t)(uint32_t)__ldg(tb.seg_off + 3 * m + 2) << 32);
+      s_sig[i] = __ldg(tb.sig + i) + fold;
+    }
   }
   // CTA-level global histogram in 32-bit counters (native shared atomics); a group that would
   // push the CTA's running step count past 2^31 first drains the counters into the global u64
@@ -1111,6 +1111,9 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   const size_t vio_bytes = !f32 ? a16((size_t)U * 8) : 0;  // fp64: the thresholds (s_thr)
   const int U4 = (U + 3) & ~3;
   const int nsegs = (int)(t.seg.size() / 4);
+  if (pen && nsegs > 0xFFFF)  // the engine then evaluates the grids in chunks
+    return "tables too large for shared memory (" + std::to_string(nsegs) +
+           " selection segments: switch counters use 16-bit indices)";
   const size_t sig_bytes = pen ? a16((size_t)M * U * 8 + (size_t)(M * 3 + 1) * 4) : 0;
   const size_t gh_bytes = a->hist ? a16((size_t)U * 4 + 4) : 0;
   // segment tables (prep_kernel): hdr [NS] u32, idle flags [M*3] i32, values [6][NS] f64 in the
