@@ -32,6 +32,10 @@ fc = cs.generate_traces(4000, 256, step_seconds=60, kind="mixed", seed=6)
 tf.evaluate(fc, 256, step_seconds=60, switch_penalty_s=10.0)
 tf.evaluate(fc, 256, step_seconds=60)
 cs.Tables.stage([fine], "f64").evaluate(fc[:600].double(), 256, step_seconds=60, switch_penalty_s=10.0)
+# ten grids (5,055 union thresholds): the warp-uniform redirect variant
+import bench  # noqa: E402
+
+cs.Tables.stage(bench.make_grids("ten"), "f32").evaluate(caps, 2000, step_seconds=60)
 t64 = cs.Tables.stage([g], "f64")
 t64.evaluate(caps.double(), 2000, step_seconds=60, switch_penalty_s=5.0)
 idx = cs.PolicyIndex(g, cs.COMBINATION)
