@@ -1164,6 +1164,9 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
           const int wpc = threads / 32;
           if (wpg > wpc) continue;
           if (tiny ? wpg != wpc : wpg == 32) continue;  // tiny: one whole-CTA group per trace
+          // ... of at most 512 threads when the trace is too short to split (C1, 1440 steps:
+          // 14.7 us per step at 512 threads, 16.8 at 1024 — staging and barriers dominate)
+          if (tiny && a->n_steps < 4096 && threads > 512) continue;
           if (force_wpg && wpg != force_wpg) continue;
           if (wpg * 32 < M * 3 + 1) continue;  // one thread per violation counter (+ the flag)
           const int gpc = wpc / wpg;
