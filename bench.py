@@ -1,13 +1,18 @@
 """Benchmark: policy-evaluated trace timesteps/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--trace-kind mixed|iid]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--trace-kind mixed|iid] [--dtype f32|f64]
     python bench.py --impl reference ...      # the reference algorithm (CPU oracle port) on host cores
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 One step = one pass of the hot path (N2 per-timestep policy kernel + N3 accumulation) over
 every timestep of the workload resident in HBM: each (trace, step) cap evaluated for all M
-grids x 3 policies, per-trace aggregates written, the global union-bin histogram reduced
-(NCCL all-reduce across ranks when N > 1). Rank 0 prints ONE JSON line.
+grids x 3 policies, per-trace aggregates written, and the sweep's statistics reduced — the
+union-bin histogram and the per-(grid, policy) sweep totals in ONE int64 NCCL all-reduce across
+ranks when N > 1. Rank 0 prints ONE JSON line.
+
+Both arms print the same ``config`` object (bench_config) and run on the same synthetic traces:
+the device generator and its host port (oracle.generate_traces) are bit-identical, so the
+reference arm times the reference algorithm on the engine arm's first traces.
 """
 
 from __future__ import annotations
@@ -16,9 +21,8 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
+import threading
 import time
 from pathlib import Path
 
@@ -27,6 +31,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "policy-evaluated trace timesteps/sec"
 UNIT = "timesteps/s"
+SEED = 2306
 
 # BASELINE.json configs; the N=1 headline is C4, the 10^6-trace sweep
 CONFIGS = {
@@ -43,16 +48,15 @@ CONFIGS = {
 }
 
 
-def make_grids(name: str):
-    import paper_2306_12247_b200 as cs
-
+def grid_params(name: str) -> list[dict]:
+    """SynthParams keyword sets of a config's grids (the reference's synthesize_grid formula;
+    the reference ships no real profiling data, so the CNN names are labels)."""
     if name == "mobilenet":
-        return [cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128, model_name="mobilenet-v1"))]
+        return [dict(mtl_cap=4, bs_cap=128, model_name="mobilenet-v1")]
     if name == "fine":
-        return [cs.synthesize_grid(cs.SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0,
-                                                  model_name="fine-8x512"))]
-    # ten documented stand-ins for the paper's CNN set (labels only: the reference ships no
-    # real profiling data); parameters drawn in the reference's random_synth_grid ranges
+        return [dict(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0, model_name="fine-8x512")]
+    # ten documented stand-ins for the paper's CNN set, parameters drawn in the reference's
+    # random_synth_grid ranges (pkg/tests/test_acceptance.py:84-98)
     import random
 
     rng = random.Random(2306_12247)
@@ -60,11 +64,16 @@ def make_grids(name: str):
              "densenet-121", "efficientnet-b0", "vgg-16", "nasnet-large"]
     out = []
     for i, n in enumerate(names):
-        out.append(cs.synthesize_grid(cs.SynthParams(
-            t_max_ips=rng.uniform(1000.0, 20000.0), tau=rng.uniform(8.0, 128.0), contention=rng.uniform(0.7, 1.0),
-            gamma=rng.uniform(0.5, 1.5), p_idle_w=rng.uniform(30.0, 100.0), p_max_w=350.0, mem_model_mb=4096.0,
-            mtl_cap=4, bs_cap=128, seed=i, model_name=n)))
+        out.append(dict(t_max_ips=rng.uniform(1000.0, 20000.0), tau=rng.uniform(8.0, 128.0),
+                        contention=rng.uniform(0.7, 1.0), gamma=rng.uniform(0.5, 1.5), p_idle_w=rng.uniform(30.0, 100.0),
+                        p_max_w=350.0, mem_model_mb=4096.0, mtl_cap=4, bs_cap=128, seed=i, model_name=n))
     return out
+
+
+def make_grids(name: str, module=None):
+    if module is None:
+        import paper_2306_12247_b200 as module
+    return [module.synthesize_grid(module.SynthParams(**p)) for p in grid_params(name)]
 
 
 def oracle_grids(grids):
@@ -78,6 +87,32 @@ def oracle_grids(grids):
         out.append(oracle.GridArrays(np.array(mtl, np.int32), np.array(bs, np.int32), np.array(thr), np.array(pw),
                                      0.0 if g.gpu_idle_power_w is None else float(g.gpu_idle_power_w)))
     return out
+
+
+def bench_config(args, cfg, world: int, union_bins: int) -> dict:
+    """The ``config`` object both arms print (identical for the same command line)."""
+    esz = 8 if args.dtype == "f64" else 4
+    return {"workload": args.config, "desc": cfg["desc"], "traces": cfg["traces"], "steps_per_trace": cfg["steps"],
+            "grids": len(grid_params(cfg["grids"])), "policies": 3, "union_bins": union_bins,
+            "step_seconds": cfg["step_seconds"], "switch_penalty_s": cfg["penalty"], "trace_kind": cfg["kind"],
+            "cap_dtype": args.dtype, "seed": SEED, "parallelism": f"trace-sharded x{world}",
+            "l2": f"inputs {cfg['traces'] * cfg['steps'] * esz / 1e9:.2f} GB "
+                  + ("> 126 MB L2 (no flush needed)" if cfg["traces"] * cfg["steps"] * esz > 126e6 * 2
+                     else "(re-read every step: L2-resident when small; C1/C2 are latency-bound)")}
+
+
+def union_bins(grids, dtype: str) -> int:
+    """Distinct power thresholds over all grids + 1 (the union bins of the staged tables; fp32
+    caps compare against fp32 round-up thresholds) — host arithmetic only."""
+    import numpy as np
+
+    pw = np.concatenate([np.asarray(g.columns()[4], np.float64) for g in grids])
+    if dtype == "f32":
+        p32 = pw.astype(np.float32)
+        up = p32.astype(np.float64) < pw
+        p32[up] = np.nextafter(p32[up], np.float32(np.inf))
+        return int(np.unique(p32).size) + 1
+    return int(np.unique(pw).size) + 1
 
 
 def dist_env():
@@ -96,56 +131,89 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
+    """NVML clocks + throttle reasons sampled every ``period_s`` on a thread during the timed
+    region (plus one sample at its start and one at its end, so even a sub-millisecond region has
+    samples taken while it ran)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("hw_power_brake_slowdown", 0x80), ("sw_power_cap", 0x4))
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.path = None
+    def __init__(self, device, period_s: float = 0.002):
+        self.device = device
+        self.period = period_s
+        self.rows = []
+        self.h = None
+        self.err = None
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.device)
+            bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001 - fall back to the ordinal
+            return pynvml.nvmlDeviceGetHandleByIndex(int(getattr(self.device, "index", self.device) or 0))
+
+    def sample(self):
+        import pynvml
+
+        if self.h is None:
+            return
+        try:
+            sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            pw = pynvml.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+            self.rows.append((time.perf_counter(), sm, rs, pw))
+        except Exception as exc:  # noqa: BLE001
+            self.err = repr(exc)[:120]
+
+    def _loop(self):
+        while not self._stop.wait(self.period):
+            self.sample()
 
     def __enter__(self):
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            self.h = self._handle()
+            import pynvml
+
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # noqa: BLE001
+            self.err = repr(exc)[:120]
+            self.h = None
+        self.sample()
+        self._thr = threading.Thread(target=self._loop, daemon=True)
+        self._thr.start()
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+        self.sample()
 
     def summary(self):
-        if not self.path or not os.path.exists(self.path):
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        rows = []
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
-                rows.append(parts)
-        os.unlink(self.path)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in rows]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for n, v in zip(names, r[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        sm = [r[1] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n, bit in self.REASONS if r[2] & bit})
+        span = self.rows[-1][0] - self.rows[0][0]
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": float(self.max_sm),
+                "reasons": reasons, "samples": len(self.rows), "span_s": round(span, 4),
+                "power_w_max": max(r[3] for r in self.rows), "source": f"NVML every {self.period * 1e3:.0f} ms"}
+
+
+def traffic_of(config: str, kind: str, dtype: str):
+    """DRAM bytes per timestep of the dominant kernel from the committed ncu --set full capture
+    of this workload (tools/ncu_summary.py --traffic-key), with the capture it came from."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text()).get(f"{config}:{kind}:{dtype}")
 
 
 def cpu_baseline(grids, caps_host, cfg, budget_s: float, threads: int | None = None):
@@ -159,23 +227,78 @@ def cpu_baseline(grids, caps_host, cfg, budget_s: float, threads: int | None = N
     S = cfg["steps"]
     threads = threads or len(os.sched_getaffinity(0))
     # calibrate on a few traces per thread (second pass, warm), then size the sample to ~budget_s
-    n0 = min(4 * threads, caps_host.shape[0])
-    calib = np.ascontiguousarray(caps_host[:n0, :S])
+    n0 = min(threads, caps_host.shape[0])
+    calib = np.ascontiguousarray(caps_host[:n0, :S], dtype=np.float32)
     for _ in range(2):
         t0 = time.perf_counter()
         oracle.simulate_batch(og, calib, cfg["step_seconds"], cfg["penalty"], threads)
         dt = max(time.perf_counter() - t0, 1e-3)
     n = int(min(caps_host.shape[0], max(n0, n0 * budget_s / dt)))
     n = max(n0, (n // threads) * threads or n0)
+    sample = np.ascontiguousarray(caps_host[:n, :S], dtype=np.float32)
     t0 = time.perf_counter()
-    _, _, _, used = oracle.simulate_batch(og, np.ascontiguousarray(caps_host[:n, :S]), cfg["step_seconds"],
-                                          cfg["penalty"], threads)
+    _, _, _, used = oracle.simulate_batch(og, sample, cfg["step_seconds"], cfg["penalty"], threads)
     wall = time.perf_counter() - t0
     return {"value": n * S / wall, "unit": UNIT, "cores": int(used), "kind": "port",
-            "sample": f"{n} traces x {S} steps x {len(grids)} grids x 3 policies ({wall:.1f}s wall, "
-                      f"{os.cpu_count()} host cpus)"}
+            "sample": f"traces 0..{n - 1} of the workload x {S} steps x {len(grids)} grids x 3 policies "
+                      f"({wall:.1f}s wall, {os.cpu_count()} host cpus)"}
 
 
+# ---- the unmodified reference package (baseline/_ref) in a process pool -------------------------
+_PY = {}
+
+
+def _py_init(ref_path: str, gname: str):
+    sys.path.insert(0, ref_path)
+    import capsim  # the reference, unmodified
+
+    _PY["capsim"] = capsim
+    _PY["grids"] = make_grids(gname, capsim)
+
+
+def _py_unit(args):
+    import datetime
+    import warnings
+
+    row, step, pen, m = args
+    capsim = _PY["capsim"]
+    tr = capsim.PowerTrace("bench", int(step), datetime.datetime(2020, 1, 1), tuple(float(x) for x in row))
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for kind in (capsim.BATCHING, capsim.MULTI_TENANT, capsim.COMBINATION):
+            capsim.simulate(_PY["grids"][m], tr, kind, switch_penalty_s=pen)
+    return time.perf_counter() - t0
+
+
+def python_reference(cfg, caps_host, budget_s: float):
+    """The reference's own simulate() (baseline/_ref, imported unmodified) over (trace, grid) units
+    of the workload, 3 policies each, in a ProcessPoolExecutor on every host core."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "capsim" / "__init__.py").exists():
+        return {"unavailable": "baseline/_ref not installed (pip install --no-deps --target baseline/_ref "
+                               "<copy of /root/reference/pkg>)"}
+    S, M = cfg["steps"], len(grid_params(cfg["grids"]))
+    workers = len(os.sched_getaffinity(0))
+    ctx = mp.get_context("spawn")
+    with cf.ProcessPoolExecutor(workers, mp_context=ctx, initializer=_py_init,
+                                initargs=(str(ref), cfg["grids"])) as ex:
+        unit = lambda i: (caps_host[i // M % caps_host.shape[0], :S], cfg["step_seconds"], cfg["penalty"], i % M)  # noqa: E731
+        t_unit = max(ex.map(_py_unit, [unit(i) for i in range(workers)]))  # warm-up + calibration
+        rounds = max(1, int(budget_s / max(t_unit, 1e-3)))
+        n = workers * rounds
+        t0 = time.perf_counter()
+        busy = sum(ex.map(_py_unit, [unit(i) for i in range(n)]))
+        wall = time.perf_counter() - t0
+    return {"value": n * S / M / wall, "unit": UNIT, "cores": workers, "kind": "reference-python",
+            "sample": f"{n} (trace, grid) units of the workload's first traces x {S} steps x 3 policies, "
+                      f"capsim.simulate from baseline/_ref ({wall:.1f}s wall, {busy / n:.2f}s per unit)"}
+
+
+# ---- engine arm -----------------------------------------------------------------------------------
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,10 +308,13 @@ def main() -> None:
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--trace-kind", default=None, help="override: solar | wind | mixed | iid")
     ap.add_argument("--traces", type=int, default=None, help="override the total trace count")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                    help="cap dtype: f32 synthetic caps, or f64 (the drop-in PowerTrace path; same caps widened)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time the host launch path instead of a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
+    ap.add_argument("--py-budget-s", type=float, default=6.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -200,14 +326,19 @@ def main() -> None:
         cfg["traces"] = args.traces
     rank, world, local = dist_env()
 
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    run_engine(args, cfg, rank, world, local)
+
+
+def run_engine(args, cfg, rank, world, local):
     import numpy as np
     import torch
 
-    if args.impl == "reference":
-        run_reference(args, cfg, rank)
-        return
-
     import paper_2306_12247_b200 as cs
+    from paper_2306_12247_b200 import _native as N
+    from paper_2306_12247_b200.shard import SweepTotals, max_over_ranks, reduce_sweep, shard_range
 
     # one rank per GPU; CAPSIM_DIST_BACKEND=gloo lets several ranks share one device (a functional
     # check of the sharded path on a single-GPU box; such timings are not bench numbers)
@@ -225,64 +356,85 @@ def main() -> None:
             dist.init_process_group(backend)
         pg = dist
     grids = make_grids(cfg["grids"])
-    tables = cs.Tables.stage(grids, "f32")
+    tables = cs.Tables.stage(grids, args.dtype)
     T_total, S = cfg["traces"], cfg["steps"]
-    # strong scaling: the configured trace population is split into contiguous shards
-    from paper_2306_12247_b200.shard import max_over_ranks, reduce_histogram, shard_range
-
+    M = len(grids)
+    U = tables.n_union_bins
+    assert U == union_bins(grids, args.dtype)
+    esz = 8 if args.dtype == "f64" else 4
+    # the configured trace population is split into contiguous shards (strong scaling); every
+    # trace is a pure function of its global id, so shards are identical whatever N is
     lo, hi = shard_range(T_total, rank, world)
     T = hi - lo
-    caps = cs.generate_traces(T, S, step_seconds=cfg["step_seconds"], kind=cfg["kind"], seed=2306,
-                              first_trace_id=lo)
+    gkw = dict(step_seconds=cfg["step_seconds"], kind=cfg["kind"], seed=SEED)
+    if args.dtype == "f32":
+        caps = cs.generate_traces(T, S, first_trace_id=lo, **gkw)
+    else:  # the same fp32 caps widened exactly to fp64, generated in slices to bound memory
+        ld = (S + 3) // 4 * 4
+        caps = torch.zeros((T, ld), dtype=torch.float64, device=dev)
+        step_t = max(1, (1 << 30) // (ld * 4))
+        for a in range(0, T, step_t):
+            b = min(T, a + step_t)
+            caps[a:b] = cs.generate_traces(b - a, S, first_trace_id=lo + a, **gkw).double()
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
 
-    # the step's launch sequence (prep, eval[, finalize]) is replayed from a CUDA graph: one graph
-    # launch per step instead of the Python/ctypes host path (which dominates C1/C2)
+    # one step = one CUDA-graph replay of [prep?, eval, finalize?, sweep totals] (one graph launch
+    # instead of the Python/ctypes host path, which dominates C1/C2) + the single collective
     ekw = dict(step_seconds=cfg["step_seconds"], switch_penalty_s=cfg["penalty"], check_violations=True,
                want_hist=True)
-    # two captured graphs with their own output buffers: step k's histogram all-reduce (a side
-    # stream, N > 1) overlaps step k+1's kernels; a buffer is reused only after its reduce is done
-    graphs = [] if args.no_graph else [tables.capture(caps, S, **ekw) for _ in range(2 if world > 1 else 1)]
+    # two captured graphs with their own output buffers: step k's all-reduce (a side stream, N > 1)
+    # overlaps step k+1's kernels; a buffer is reused only after its reduce is done
+    graphs = [] if args.no_graph else [tables.capture(caps, S, sweep_totals=True, **ekw)
+                                       for _ in range(2 if world > 1 else 1)]
     side = torch.cuda.Stream() if world > 1 else None
     reduced = [None, None]  # event: that buffer's all-reduce finished
     nstep = [0]
+    rows = M * 3
+    hist_n = U if (graphs and graphs[0].result.hist is not None) else 0
+    bufs = [torch.zeros(hist_n + rows * N.CS_SWEEP_WORDS, dtype=torch.int64, device=dev) for _ in range(2)]
 
     def step():
         k = nstep[0] % max(1, len(graphs))
         nstep[0] += 1
         if reduced[k] is not None:
             stream.wait_event(reduced[k])
-        r = graphs[k].replay() if graphs else tables.evaluate(caps, S, **ekw)
+        if graphs:
+            g = graphs[k]
+            r, words = g.replay(), g.words
+        else:
+            r = tables.evaluate(caps, S, **ekw)
+            words = cs.sweep_words(tables, r.agg)
+        buf = bufs[k]
         if side is None:
-            reduce_histogram(r.hist)  # single rank: a no-op
-            return r
+            return r, words, None
         done = torch.cuda.Event()
         done.record(stream)
         side.wait_event(done)
         with torch.cuda.stream(side):
-            reduce_histogram(r.hist)  # the single collective: global config histogram (int64, NCCL)
+            if hist_n:
+                buf[:hist_n].copy_(r.hist)
+            buf[hist_n:].copy_(words.view(-1))
+            reduce_sweep(buf)  # the single collective: [histogram | sweep totals], int64 SUM
             ev = torch.cuda.Event()
             ev.record(side)
         reduced[k] = ev
-        return r
+        return r, words, buf
 
     for _ in range(args.warmup):
-        res = step()
+        res, words, buf = step()
     if side is not None:
         stream.wait_stream(side)
     torch.cuda.synchronize()
-    launches_per_step = tables.launch_count()
+    launches_per_step = tables.launch_count() + 1  # + the sweep-totals kernel
     if pg is not None:
         pg.barrier()
     torch.cuda.synchronize()
-    kern_ms = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            res = step()
-            kern_ms.append(None)
+            res, words, buf = step()
         if side is not None:
             stream.wait_stream(side)  # the last reduce belongs to the timed region
         ev1.record(stream)
@@ -294,12 +446,9 @@ def main() -> None:
     # dominant kernel: time it alone with the library's own launch events (same stream)
     import ctypes as C
 
-    from paper_2306_12247_b200 import _native as N
-
     single = []
     for _ in range(max(3, min(args.steps, 10))):
-        tables.evaluate(caps, S, step_seconds=cfg["step_seconds"], switch_penalty_s=cfg["penalty"],
-                        check_violations=True, want_hist=True)
+        tables.evaluate(caps, S, **ekw)
         torch.cuda.synchronize()
         ms = C.c_float()
         N.check(N.lib().cs_eval_last_kernel_ms(C.byref(ms)))
@@ -311,28 +460,31 @@ def main() -> None:
     ms_per_step = elapsed_ms / args.steps
     value = T_total * S / (ms_per_step / 1e3)
 
-    # correctness gate on the measured data: violations 0, and a sampled parity check
-    viol = int(res.violations.sum())
-    hist_total = int(res.hist.sum())
-    assert hist_total == T_total * S, (hist_total, T_total * S)
+    # the reduced sweep statistics (identical at any N: integer words only)
+    if buf is None:
+        gh = res.hist.cpu().numpy() if hist_n else None
+        gw = words.cpu().numpy()
+    else:
+        host = buf.cpu().numpy()
+        gh, gw = (host[:hist_n] if hist_n else None), host[hist_n:].reshape(rows, N.CS_SWEEP_WORDS)
+    totals = SweepTotals(gw.reshape(rows, N.CS_SWEEP_WORDS), T_total, tuple(g.model_name for g in grids))
+    # correctness gates on the measured data
+    viol = sum(totals.violations(m, p) for m in range(M) for p in range(3))
     assert viol == 0
-    sweep = sweep_summary(tables, res.hist, cfg) if rank == 0 else None
+    assert all(totals.steps(m, p) == T_total * S for m in range(M) for p in range(3))
+    if gh is not None:
+        assert int(gh.sum()) == T_total * S, (int(gh.sum()), T_total * S)
 
-    M = len(grids)
-    bytes_per_launch = T * S * 4 + T * M * 3 * 48 + tables.n_union_bins * 8
+    bytes_per_launch = T * S * esz + T * M * 3 * 48 + U * 8
     achieved_gbs = bytes_per_launch / (kernel_ms / 1e3) / 1e9
     peak, peak_src = peaks()
-    # DRAM bytes per launch from the committed ncu --set full capture of this workload
-    # (tools/ncu_summary.py --traffic-key), scaled from bytes per timestep to this launch
-    traffic = None
-    tpath = ROOT / "profiles" / "ncu_traffic.json"
-    if tpath.exists():
-        tdoc = json.loads(tpath.read_text()).get(f"{args.config}:{cfg['kind']}")
-        if tdoc:
-            traffic = tdoc["dram_bytes_per_timestep"] * T * S
+    tr = traffic_of(args.config, cfg["kind"], args.dtype)
+    traffic = tr["dram_bytes_per_timestep"] * T * S if tr else None
 
     out = None
     if rank == 0:
+        import hashlib
+
         out = {
             "metric": METRIC,
             "value": value,
@@ -344,88 +496,85 @@ def main() -> None:
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f32 caps / f64 sums",
+            "dtype": f"{args.dtype} caps / f64 sums",
             "data": f"synthetic {cfg['kind']} traces (counter-based RNG keyed by global trace id), "
                     "synthetic grids (reference synthesize_grid formula)",
-            "config": {"workload": args.config, "desc": cfg["desc"], "traces": T_total, "steps_per_trace": S,
-                       "grids": M, "policies": 3, "union_bins": tables.n_union_bins,
-                       "step_seconds": cfg["step_seconds"], "switch_penalty_s": cfg["penalty"],
-                       "trace_kind": cfg["kind"], "parallelism": f"trace-sharded x{world}",
-                       "launch": ("cuda-graph replay" + (" x2, reduce overlapped" if side is not None else ""))
-                       if graphs else "host path",
-                       "dist_backend": backend if world > 1 else None,
-                       "l2": f"inputs {T_total * S * 4 / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
-                       "policy_evaluations_per_step": T_total * S * M * 3, "plan": plan},
+            "config": bench_config(args, cfg, world, U),
+            "plan": plan,
+            "launch": ("cuda-graph replay" + (" x2, reduce overlapped" if side is not None else ""))
+            if graphs else "host path",
+            "dist_backend": backend if world > 1 else None,
+            "policy_evaluations_per_step": T_total * S * M * 3,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
+                         "traffic_source": (f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
+                                            f"{tr['kernel']} ({tr['source']}): {tr['dram_bytes_per_timestep']:.4f} "
+                                            "B/timestep x this launch's timesteps") if tr else None,
                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured"
                          else "fallback 6.65 TB/s (B200_PROFILING.md)",
-                         "algorithmic_bytes_per_launch": bytes_per_launch, "kernel_ms": kernel_ms,
-                         "kernel": "eval_kernel<float,...>"},
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "algorithmic_bytes_per_timestep": bytes_per_launch / (T * S), "kernel_ms": kernel_ms,
+                         "kernel": f"eval_kernel<{'float' if args.dtype == 'f32' else 'double'},...>"},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
+            "sweep": {"hist_sha256": hashlib.sha256(gh.astype("<i8").tobytes()).hexdigest()[:16]
+                      if gh is not None else None,
+                      "totals_sha256": hashlib.sha256(gw.astype("<i8").tobytes()).hexdigest()[:16],
+                      "grids": totals.summary(max_grids=3)},
         }
         if world > 1:
             out["rank_max_kernel_ms"] = kernel_ms_max
 
     # ---- e2e: same metric through the C-ABI host-buffer path (pinned H2D + D2H in the region) ----
-    host = torch.empty((T, caps.shape[1]), dtype=torch.float32, pin_memory=True)
-    host.copy_(caps)
-    del caps
+    # every rank keeps its shard in pinned host memory (bounded by the host's free memory: when the
+    # shard does not fit, e2e runs over its first traces and says so); rank 0 also feeds the CPU
+    # baselines and the parity sample from it
+    row_b = caps.shape[1] * caps.element_size()
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 1 << 40
+    n_host = T if not args.no_e2e else (min(T, 1 << 16) if rank == 0 else 0)
+    n_host = int(min(n_host, max(1, 0.6 * avail / world // row_b)))
+    host = None
+    if n_host:
+        host = torch.empty((n_host, caps.shape[1]), dtype=caps.dtype, pin_memory=True)
+        host.copy_(caps[:n_host])
+    ref_agg = res.agg[:64].cpu()
+    del caps, graphs
     torch.cuda.empty_cache()
     if not args.no_e2e:
         try:
-            e2e = run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=res.agg[:64])
+            e2e = run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=ref_agg)
             if rank == 0:
                 out["e2e"] = e2e
         except Exception as exc:  # keep the device-side line even if the host path fails
             if rank == 0:
                 out["e2e"] = {"value": None, "unit": UNIT, "error": repr(exc)[:300]}
 
-    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N=1 only
-        out["cpu_baseline"] = cpu_baseline(grids, host.numpy(), cfg, args.cpu_budget_s)
     if rank == 0:
+        caps32 = host.numpy() if args.dtype == "f32" else host.numpy().astype(np.float32)  # exact: widened f32
+        if world == 1 and not args.no_cpu:  # the CPU baselines: rank 0 at N=1 only
+            out["cpu_baseline"] = cpu_baseline(grids, caps32, cfg, args.cpu_budget_s)
+            try:
+                out["cpu_baseline"]["python_reference"] = python_reference(cfg, caps32, args.py_budget_s)
+            except Exception as exc:  # noqa: BLE001
+                out["cpu_baseline"]["python_reference"] = {"unavailable": repr(exc)[:200]}
         # sampled parity on the benchmarked data (bit-exact idle counts, 1e-6 sums)
         from oracle import oracle
 
-        sample_np = host.numpy()
         k = min(8, T)
-        avg, idle, en, _ = oracle.simulate_batch(oracle_grids(grids), np.ascontiguousarray(sample_np[:k, :S]),
+        avg, idle, en, _ = oracle.simulate_batch(oracle_grids(grids), np.ascontiguousarray(caps32[:k, :S]),
                                                  cfg["step_seconds"], cfg["penalty"])
-        g = res.agg[:k].cpu()
+        g = ref_agg[:k]
         ok = bool(np.array_equal(g.view(torch.int64)[..., 2].numpy(), idle)
                   and np.allclose(g[..., 0].numpy(), avg, rtol=1e-6, atol=0)
                   and np.allclose(g[..., 1].numpy(), en, rtol=1e-6, atol=0))
-        out["sweep"] = sweep
         out["parity_sample"] = {"traces": k, "ok": ok, "violations": viol,
                                 "bit_exact_avg": bool(np.array_equal(g[..., 0].numpy(), avg))}
-    if rank == 0:
         print(json.dumps(out))
     if pg is not None:
         pg.destroy_process_group()
-
-
-def sweep_summary(tables, hist, cfg):
-    """Sweep-level statistics from the reduced union-bin histogram (the one collective): per grid
-    and policy the share of idle steps and the mean per-step throughput over every trace (exact
-    integer counts, fsum on the host). Identical at any GPU count; ``hist_sha256`` makes that
-    checkable across the scaling runs. Penalty-free values (switched steps are per trace)."""
-    import hashlib
-    import math
-
-    h = hist.cpu().numpy()
-    out = {"hist_sha256": hashlib.sha256(h.astype("<i8").tobytes()).hexdigest()[:16], "grids": []}
-    for m, rows in enumerate(tables.config_histograms(h)):
-        g = tables.grids[m]
-        per = {}
-        for p, d in zip(("batching", "multi-tenant", "combination"), rows):
-            n = sum(d.values())
-            thr = math.fsum(c * g.entries[k].throughput_ips for k, c in d.items() if k is not None)
-            per[p] = {"mean_throughput_ips": thr / n, "idle_fraction": d.get(None, 0) / n}
-        out["grids"].append({"model": g.model_name, **per})
-        if m >= 2:
-            break  # first grids only: keeps the line short
-    return out
 
 
 def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=None):
@@ -435,7 +584,8 @@ def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=None):
     import torch
 
     T = host.shape[0]
-    chunk = max(1, min(T, (1 << 30) // (host.shape[1] * 4)))
+    esz = host.element_size()
+    chunk = max(1, min(T, (1 << 30) // (host.shape[1] * esz)))
     eng = cs.HostEngine(tables, chunk_traces=chunk, n_steps_max=S)
     agg_h = torch.empty((T, M, 3, 6), dtype=torch.float64, pin_memory=True)
     hist_h = torch.empty(tables.n_union_bins, dtype=torch.int64, pin_memory=True)
@@ -452,39 +602,45 @@ def run_e2e(cs, tables, host, cfg, S, M, args, pg, dev, T_total, ref_agg=None):
     ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps, dev)
     # the host path must reproduce the device path's aggregates exactly (same kernel, same data)
     k = min(64, T)
-    same = bool(torch.equal(agg_h[:k], ref_agg[:k].cpu())) if ref_agg is not None else None
+    same = bool(torch.equal(agg_h[:k], ref_agg[:k])) if ref_agg is not None else None
     world = pg.get_world_size() if pg is not None else 1
-    if world > 1:  # whole-job bytes, like the value (every rank moves its own shard)
-        t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+    T_e2e = T
+    if world > 1:  # whole-job traces and bytes, like the value (every rank moves its own shard)
+        t = torch.tensor([float(h2d), float(d2h), float(T)], dtype=torch.float64, device=dev)
         pg.all_reduce(t)
-        h2d, d2h = int(t[0].item()), int(t[1].item())
-    return {"value": T_total * S / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": e_steps, "matches_device_path": same,
+        h2d, d2h, T_e2e = int(t[0].item()), int(t[1].item()), int(t[2].item())
+    return {"value": T_e2e * S / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": ms, "steps": e_steps, "matches_device_path": same, "traces": T_e2e,
             "path": f"cs_engine_eval_host: pinned host caps, H2D/eval/D2H on 3 streams, {chunk}-trace chunks"}
 
 
-def run_reference(args, cfg, rank):
-    """The reference algorithm on the box's host cores (oracle port, all threads); rank 0 only."""
+# ---- reference arm --------------------------------------------------------------------------------
+def run_reference(args, cfg, rank, world):
+    """The reference algorithm (oracle port: PolicyIndex bisect + _aggregate fsum, all 3 policies,
+    pthreads over traces) on all host cores, on the engine arm's own first traces (host port of
+    the generator, bit-identical); rank 0 only. Also states the unmodified Python reference."""
     import numpy as np
+
+    from oracle import oracle
 
     if rank != 0:
         return
-    from oracle import oracle
-
     grids = make_grids(cfg["grids"])
     og = oracle_grids(grids)
     S = cfg["steps"]
     threads = len(os.sched_getaffinity(0))
-    # host-generated traces of the same shape (the reference arm must not touch the GPU)
-    rng = np.random.default_rng(2306)
-    n = threads
-    base = np.clip(np.cumsum(rng.normal(0, 6.0, (n, S)), axis=1) + rng.uniform(50, 300, (n, 1)), 0, 350)
-    caps = np.ascontiguousarray(base.astype(np.float32))
+    U = union_bins(grids, args.dtype)
+    gen = lambda n: oracle.generate_traces(n, S, step_seconds=cfg["step_seconds"], kind=cfg["kind"], seed=SEED,  # noqa: E731
+                                           n_threads=threads)[:, :S]
+    # size each step to ~2 s of work: calibrate on one trace per thread
+    n = min(cfg["traces"], threads)
+    caps = np.ascontiguousarray(gen(n))
     t0 = time.perf_counter()
     oracle.simulate_batch(og, caps, cfg["step_seconds"], cfg["penalty"], threads)
     dt = time.perf_counter() - t0
-    reps = max(1, int(3.0 / max(dt, 1e-3)))
-    caps = np.ascontiguousarray(np.tile(caps, (reps, 1)))
+    n = int(min(cfg["traces"], max(n, n * 2.0 / max(dt, 1e-3))))
+    n = max(min(threads, cfg["traces"]), n // threads * threads)
+    caps = np.ascontiguousarray(gen(n))
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -492,18 +648,24 @@ def run_reference(args, cfg, rank):
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     per_step = statistics.mean(times)
-    value = caps.shape[0] * S / per_step
-    sample = f"{caps.shape[0]} traces x {S} steps x {len(grids)} grids x 3 policies per step"
-    print(json.dumps({
+    value = n * S / per_step
+    sample = (f"traces 0..{n - 1} of the workload (the engine arm's own caps, host generator port) x {S} steps x "
+              f"{len(grids)} grids x 3 policies per step")
+    line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64 (reference algorithm)",
-        "data": "synthetic random-walk traces (host)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "traces": cfg["traces"], "steps_per_trace": S,
-                   "grids": len(grids), "policies": 3},
+        "data": f"synthetic {cfg['kind']} traces (counter-based RNG keyed by global trace id), "
+                "synthetic grids (reference synthesize_grid formula)",
+        "config": bench_config(args, cfg, world, U),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(used), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    }
+    try:
+        line["cpu_baseline"]["python_reference"] = python_reference(cfg, caps, args.py_budget_s)
+    except Exception as exc:  # noqa: BLE001
+        line["cpu_baseline"]["python_reference"] = {"unavailable": repr(exc)[:200]}
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":

@@ -151,8 +151,23 @@ typedef struct {
   int32_t trace_segments; /* > 1: long traces split across worker groups (+ finalize kernel) */
   int32_t lut_entries, lut_shift;
   int32_t epilogue;       /* 0 segment tables from global, 1 staged segment tables, 2 per-bin */
+  int32_t redirect_uniform; /* 1: the warp-uniform redirect kernel variant (redirect-heavy fp32 LUTs) */
 } cs_eval_plan;
 int cs_eval_last_plan(cs_eval_plan* out);
+
+/* ---- sweep totals (the aggregate statistics of a sharded Monte Carlo sweep) ----
+ * Per (grid, policy) row of agg_dev [n_traces][n_rows] (n_rows = n_grids * 3), CS_SWEEP_WORDS u64:
+ *   [0] steps  [1] idle steps  [2] switched steps  [3] violations
+ *   [4..7]  sum over traces of avg_throughput_ips  } exact 128-bit fixed point (LSB 2^-50) as four
+ *   [8..11] sum over traces of energy_proxy_wh     } 32-bit limbs, each summed separately in u64
+ * Every word is an integer sum, so the cross-GPU reduction is one int64 SUM all-reduce (NCCL) or
+ * peer-memory atomics, and the totals do not depend on how traces were sharded; the host
+ * recombines value = (sum_k limb_k 2^(32k)) / 2^50 exactly and rounds once.
+ * flags: CS_FLAG_ACCUMULATE_HIST adds into totals_dev instead of overwriting it (it may then
+ * point into another device's memory with peer access enabled). */
+#define CS_SWEEP_WORDS 12
+int cs_sweep_totals(const cs_agg* agg_dev, int64_t n_traces, int32_t n_rows, uint64_t* totals_dev, uint32_t flags,
+                    void* stream);
 
 /* ---- per-cap API: select_config (policy.py:172-188) and feasible_set (policy.py:151-169) as
  *      warp-per-query argmax (shuffle) / ballot kernels over the grid's raw entries ---- */

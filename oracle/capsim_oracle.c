@@ -20,6 +20,8 @@
  *   ora_simulate        sim.py:130-188      (simulate: per-step selection + aggregate)
  *   ora_simulate_batch  loops ora_simulate over (trace, grid, policy) with pthreads — the
  *                       CPU baseline ("port") the bench times beside the GPU.
+ *   ora_generate_traces not a reference function: host port of the bench's synthetic trace
+ *                       generator, so the reference arm runs on the engine arm's exact caps.
  */
 #include <math.h>
 #include <pthread.h>
@@ -572,4 +574,122 @@ int32_t ora_select_sampling(const int32_t* mtl, const int32_t* bs, const double*
     cur = move;
   }
   return cur;
+}
+
+/* ---- bench input generator (not a reference function) ------------------------------------
+ * Host restatement of gen_kernel (paper_2306_12247_b200/csrc/aux_kernels.cu): the synthetic
+ * solar / wind / iid cap traces of BASELINE.json's configs, a pure function of
+ * (seed, global trace id). Every operation is exactly rounded IEEE fp32 or integer (built with
+ * -ffp-contract=off; the kernel with -fmad=false), so this produces the device's traces bit for
+ * bit and bench.py's reference arm times the reference algorithm on the engine arm's inputs. */
+#define ORA_TRACE_SOLAR 0
+#define ORA_TRACE_WIND 1
+#define ORA_TRACE_MIXED 2
+#define ORA_TRACE_IID 3
+#define ORA_GEN_CHUNK 4096
+
+static uint64_t ora_splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+static float ora_u01(uint64_t h) { return (float)(h >> 40) * (1.0f / 16777216.0f); }
+static float ora_gauss(uint64_t h) {
+  const float s = ora_u01(h) + ora_u01(h * 0x9E3779B97F4A7C15ull) + ora_u01(ora_splitmix(h)) +
+                  ora_u01(ora_splitmix(h ^ 0xABCDull));  /* Irwin-Hall(4), unit variance */
+  return (s - 2.0f) * 1.7320508f;
+}
+static float ora_clear_sky(float x) {
+  const float w = 2.0f * x - 1.0f, z = w * w;
+  float p = -2.52020424e-05f;
+  p = p * z + 9.19260275e-04f;
+  p = p * z - 2.08634808e-02f;
+  p = p * z + 2.53669508e-01f;
+  p = p * z - 1.23370055f;
+  return p * z + 1.0f;
+}
+
+static void ora_generate_one(float* row, int64_t S, int64_t tid, int32_t step_seconds, int32_t kind, float peak,
+                             uint64_t seed, float a_cloud) {
+  const uint64_t hk = ora_splitmix(seed ^ ora_splitmix((uint64_t)tid));
+  int k = kind;
+  if (k == ORA_TRACE_MIXED) k = (tid & 1) ? ORA_TRACE_WIND : ORA_TRACE_SOLAR;
+  const float var = 0.1f + 0.7f * ora_u01(ora_splitmix(hk ^ 1));
+  const float phase = 86400.0f * ora_u01(ora_splitmix(hk ^ 2));
+  const float dt = (float)step_seconds;
+  const float wind_mu = 5.0f + 5.0f * ora_u01(ora_splitmix(hk ^ 3));
+  const float theta = 1.0f / 7200.0f;
+  const float cloud_sd = var * 0.5f * sqrtf(fmaxf(1.0f - a_cloud * a_cloud, 1e-6f));
+  const float sdt = fminf(theta * dt, 1.0f);
+  const float wind_sd = var * 4.0f * sqrtf(2.0f * sdt);
+  for (int64_t c0 = 0; c0 < S; c0 += ORA_GEN_CHUNK) {
+    const int64_t c1 = c0 + ORA_GEN_CHUNK < S ? c0 + ORA_GEN_CHUNK : S;
+    const uint64_t hc = ora_splitmix(hk ^ (0xC0FFEEull + (uint64_t)(c0 / ORA_GEN_CHUNK)));
+    float cloud = fminf(fmaxf(0.7f + var * 0.5f * ora_gauss(hc), 0.2f), 1.0f);
+    float wind = fmaxf(wind_mu + var * 4.0f * 0.7f * ora_gauss(ora_splitmix(hc)), 0.0f);
+    for (int64_t s = c0; s < c1; ++s) {
+      const uint64_t hs = ora_splitmix(hk ^ (uint64_t)(s * 0x632BE59BD9B4E019ull));
+      float v;
+      if (k == ORA_TRACE_IID) {
+        v = peak * ora_u01(hs);
+      } else if (k == ORA_TRACE_SOLAR) {
+        const float tod = fmodf(phase + (float)s * dt, 86400.0f) / 3600.0f;
+        const float clear = (tod > 6.0f && tod < 18.0f) ? ora_clear_sky((tod - 6.0f) / 12.0f) : 0.0f;
+        cloud = a_cloud * cloud + (1.0f - a_cloud) * 0.7f + cloud_sd * ora_gauss(hs);
+        cloud = fminf(fmaxf(cloud, 0.2f), 1.0f);
+        v = peak * clear * cloud;
+      } else {
+        wind = wind + sdt * (wind_mu - wind) + wind_sd * ora_gauss(hs);
+        wind = fmaxf(wind, 0.0f);
+        float f = 0.0f;
+        if (wind >= 3.0f && wind < 25.0f) {
+          const float r = (wind - 3.0f) / 9.0f;
+          f = wind >= 12.0f ? 1.0f : r * r * r;
+        }
+        v = peak * f;
+      }
+      row[s] = fminf(fmaxf(v, 0.0f), peak);
+    }
+  }
+}
+
+typedef struct {
+  float* caps;
+  int64_t T, S, ld, first_id, next;
+  int32_t step_seconds, kind;
+  float peak, a_cloud;
+  uint64_t seed;
+  pthread_mutex_t mu;
+} ora_gen_job;
+
+static void* ora_gen_worker(void* arg) {
+  ora_gen_job* j = (ora_gen_job*)arg;
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    const int64_t t = j->next++;
+    pthread_mutex_unlock(&j->mu);
+    if (t >= j->T) break;
+    ora_generate_one(j->caps + t * j->ld, j->S, j->first_id + t, j->step_seconds, j->kind, j->peak, j->seed,
+                     j->a_cloud);
+  }
+  return NULL;
+}
+
+/* caps: [T][ld] fp32 (columns >= S untouched). Same arguments as cs_generate_traces. */
+int ora_generate_traces(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
+                        int32_t kind, float peak, uint64_t seed, int n_threads) {
+  if (T < 0 || S < 0 || ld < S || step_seconds <= 0 || kind < 0 || kind > 3) return -1;
+  ora_gen_job j;
+  j.caps = caps; j.T = T; j.S = S; j.ld = ld; j.first_id = first_id; j.next = 0;
+  j.step_seconds = step_seconds; j.kind = kind; j.peak = peak; j.seed = seed;
+  j.a_cloud = (float)exp(-(double)step_seconds / 3600.0);
+  pthread_mutex_init(&j.mu, NULL);
+  if (n_threads < 1) n_threads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)n_threads);
+  for (int i = 0; i < n_threads; ++i) pthread_create(&th[i], NULL, ora_gen_worker, &j);
+  for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+  pthread_mutex_destroy(&j.mu);
+  free(th);
+  return 0;
 }

@@ -92,6 +92,9 @@ def lib():
         L.ora_select_sampling.argtypes = [i32p, i32p, f64p, f64p, C.c_int, C.c_int64, C.c_int64, C.c_double, u32p,
                                           C.c_int, C.POINTER(C.c_int64)]
         L.ora_select_sampling.restype = C.c_int32
+        L.ora_generate_traces.argtypes = [f32p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                          C.c_float, C.c_uint64, C.c_int]
+        L.ora_generate_traces.restype = C.c_int
         _lib = L
     return _lib
 
@@ -174,6 +177,24 @@ def simulate_batch(grids: list[GridArrays], caps2d: np.ndarray, step_seconds: in
                                     float(switch_penalty_s), int(n_threads), out_avg, out_idle, out_en)
     shp = (t, m, 3)
     return out_avg.reshape(shp), out_idle.reshape(shp), out_en.reshape(shp), used
+
+
+TRACE_KINDS = {"solar": 0, "wind": 1, "mixed": 2, "iid": 3}
+
+
+def generate_traces(n_traces: int, n_steps: int, *, step_seconds: int, kind: str = "mixed", peak_w: float = 350.0,
+                    seed: int = 1, first_trace_id: int = 0, ld: int | None = None, n_threads: int | None = None):
+    """Host port of the engine's synthetic trace generator (cs_generate_traces): bit-identical
+    float32 [n_traces, ld] caps for the same arguments (bench inputs, not a reference function)."""
+    ld = ld if ld is not None else (n_steps + 3) // 4 * 4
+    out = np.zeros((n_traces, ld), dtype=np.float32)
+    if n_threads is None:
+        n_threads = len(os.sched_getaffinity(0))
+    rc = lib().ora_generate_traces(out, n_traces, n_steps, ld, first_trace_id, int(step_seconds), TRACE_KINDS[kind],
+                                   float(peak_w), int(seed) & (2**64 - 1), int(n_threads))
+    if rc != 0:
+        raise ValueError("bad generator arguments")
+    return out
 
 
 def seed_key(seed: int) -> np.ndarray:

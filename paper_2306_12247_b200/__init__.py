@@ -38,6 +38,7 @@ from .columnar import (
     table_to_reports,
 )
 from .engine import EvalResult, HostEngine, Tables, generate_traces
+from .shard import ShardedResult, SweepTotals, evaluate_sharded, shard_range, sweep_words
 from .errors import CapsimError, ParseError, ValidationError
 from .policy import (
     BATCHING,
@@ -113,7 +114,8 @@ __all__ = [
     "report_from_dict", "report_json_text", "report_to_dict", "sampling_policy", "sampling_steps", "save_grid", "save_report",
     "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
     "slice_report", "synthesize_grid", "trace_array", "trace_csv_text", "trace_stats",
-    "Tables", "EvalResult", "HostEngine", "generate_traces", "TraceMatrix", "load_traces", "load_trace_matrix",
+    "Tables", "EvalResult", "HostEngine", "generate_traces", "TraceMatrix",
+    "ShardedResult", "SweepTotals", "evaluate_sharded", "shard_range", "sweep_words", "load_traces", "load_trace_matrix",
     "ColumnarRun", "eval_table", "histogram_table", "load_columnar", "reports_table", "save_columnar", "steps_table",
     "table_to_reports",
     "REACTIVE", "ControlEvent", "ControllerReport", "ControllerState", "ControlMode", "EventKind",

@@ -31,6 +31,8 @@ CS_FLAG_PREPARED = 8
 
 CS_CTRL_TIME_MAJOR = 256
 
+CS_SWEEP_WORDS = 12
+
 CS_QUERY_BINS = 0
 CS_QUERY_SELECT = 1
 CS_QUERY_FEASIBLE = 2
@@ -45,7 +47,7 @@ EXPORTS = (
     "cs_eval_workspace_size", "cs_eval", "cs_eval_last_kernel_ms", "cs_eval_last_launches", "cs_eval_last_plan",
     "cs_select_caps", "cs_feasible_caps", "cs_query_host",
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
-    "cs_replay", "cs_generate_traces", "cs_select_sampling", "cs_entries_aggregate",
+    "cs_sweep_totals", "cs_replay", "cs_generate_traces", "cs_select_sampling", "cs_entries_aggregate",
     "cs_traces_parse_files", "cs_traces_parse_text", "cs_traces_info", "cs_traces_copy", "cs_traces_pack",
     "cs_traces_destroy",
 )
@@ -123,7 +125,7 @@ class EvalArgs(C.Structure):
 
 class EvalPlan(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("ctas", "threads", "warps_per_group", "smem_bytes", "trace_segments",
-                                         "lut_entries", "lut_shift", "epilogue")]
+                                         "lut_entries", "lut_shift", "epilogue", "redirect_uniform")]
 
 
 class TraceInfo(C.Structure):
@@ -173,6 +175,7 @@ def _declare(L: C.CDLL) -> None:
         "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),
         "cs_select_sampling": ([vp, i32, vp, i64, i64, i64, i64, i64, C.c_uint64, i64, vp, vp, vp], C.c_int),
         "cs_query_host": ([vp, i32, i32, i32, vp, i64, vp, vp], C.c_int),
+        "cs_sweep_totals": ([vp, i64, i32, vp, u32, vp], C.c_int),
         "cs_entries_aggregate": ([vp, i64, i64, i64, vp, i32, dbl, vp, vp, vp, vp], C.c_int),
         "cs_traces_parse_files": ([P(C.c_char_p), i32, i64, i32, i32, P(vp)], C.c_int),
         "cs_traces_parse_text": ([C.c_char_p, i64, i64, i32, P(vp)], C.c_int),

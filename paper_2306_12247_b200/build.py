@@ -20,7 +20,7 @@ LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libcapsim_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["staging.cpp", "capi.cpp", "eval.cu", "aux_kernels.cu", "replay.cu", "sampling.cu", "ingest.cpp"]
+SOURCES = ["staging.cpp", "capi.cpp", "eval.cu", "aux_kernels.cu", "replay.cu", "sampling.cu", "sweep.cu", "ingest.cpp"]
 HEADERS = ["cs_internal.h", "cs_mt.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

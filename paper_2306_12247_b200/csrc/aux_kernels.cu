@@ -110,15 +110,31 @@ __device__ __forceinline__ float gauss(uint64_t h) {
   return (s - 2.0f) * 1.7320508f;
 }
 
+// Clear-sky curve sin(pi * x) on [0, 1] as cos(pi * w / 2), w = 2x - 1, by its Taylor polynomial
+// in z = w^2 through z^5 (|error| < 5e-7): only IEEE fp32 multiplies and adds (the build uses
+// -fmad=false), so the host restatement (oracle/capsim_oracle.c: ora_generate_traces) reproduces
+// every sample bit for bit.
+__device__ __forceinline__ float clear_sky(float x) {
+  const float w = 2.0f * x - 1.0f, z = w * w;
+  float p = -2.52020424e-05f;          // (-1)^k pi^2k / ((2k)! 4^k), k = 5 .. 1
+  p = p * z + 9.19260275e-04f;
+  p = p * z - 2.08634808e-02f;
+  p = p * z + 2.53669508e-01f;
+  p = p * z - 1.23370055f;
+  return p * z + 1.0f;
+}
+
 // One warp generates 32 traces (a lane each, sequential in time) over one chunk of
 // kGenChunk steps and writes 32x32 tiles transposed through shared memory so every store is a
 // coalesced 128-byte row segment. Chunks run in parallel (blockIdx.y); each starts its AR(1) /
 // OU state from a draw keyed by (seed, trace id, chunk), so the traces stay a pure function of
-// the global trace id.
+// the global trace id. Every operation is exactly rounded IEEE fp32 (no intrinsics, no
+// contraction), so the host port produces identical traces (the reference arm of bench.py times
+// the reference algorithm on exactly these caps).
 constexpr int64_t kGenChunk = 4096;
 
 __global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
-                           int32_t kind, float peak, uint64_t seed) {
+                           int32_t kind, float peak, uint64_t seed, float a_cloud) {
   __shared__ float tile[8][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + w) * 32;
@@ -132,9 +148,11 @@ __global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_
   const float var = 0.1f + 0.7f * u01(splitmix(hk ^ 1));           // Table-1 variation range 10%..80%
   const float phase = 86400.0f * u01(splitmix(hk ^ 2));            // start time of day offset
   const float dt = (float)step_seconds;
-  const float a_cloud = __expf(-dt / 3600.0f);                      // 1 h cloud correlation time
   const float wind_mu = 5.0f + 5.0f * u01(splitmix(hk ^ 3));       // mean wind speed (m/s)
   const float theta = 1.0f / 7200.0f;                               // OU mean reversion (1/s)
+  const float cloud_sd = var * 0.5f * sqrtf(fmaxf(1.0f - a_cloud * a_cloud, 1e-6f));
+  const float sdt = fminf(theta * dt, 1.0f);
+  const float wind_sd = var * 4.0f * sqrtf(2.0f * sdt);
   const uint64_t hc = splitmix(hk ^ (0xC0FFEEull + (uint64_t)blockIdx.y));
   float cloud = fminf(fmaxf(0.7f + var * 0.5f * gauss(hc), 0.2f), 1.0f);
   float wind = fmaxf(wind_mu + var * 4.0f * 0.7f * gauss(splitmix(hc)), 0.0f);
@@ -147,17 +165,18 @@ __global__ void gen_kernel(float* caps, int64_t T, int64_t S, int64_t ld, int64_
         v = peak * u01(hs);
       } else if (k == CS_TRACE_SOLAR) {
         const float tod = fmodf(phase + (float)s * dt, 86400.0f) / 3600.0f;
-        const float clear = (tod > 6.0f && tod < 18.0f) ? __sinf(3.14159265f * (tod - 6.0f) / 12.0f) : 0.0f;
-        cloud = a_cloud * cloud + (1.0f - a_cloud) * 0.7f +
-                var * 0.5f * sqrtf(fmaxf(1.0f - a_cloud * a_cloud, 1e-6f)) * gauss(hs);
+        const float clear = (tod > 6.0f && tod < 18.0f) ? clear_sky((tod - 6.0f) / 12.0f) : 0.0f;
+        cloud = a_cloud * cloud + (1.0f - a_cloud) * 0.7f + cloud_sd * gauss(hs);  // 1 h AR(1) cloud factor
         cloud = fminf(fmaxf(cloud, 0.2f), 1.0f);
         v = peak * clear * cloud;
       } else {
-        const float sdt = fminf(theta * dt, 1.0f);
-        wind = wind + sdt * (wind_mu - wind) + var * 4.0f * sqrtf(2.0f * sdt) * gauss(hs);
+        wind = wind + sdt * (wind_mu - wind) + wind_sd * gauss(hs);  // OU wind speed
         wind = fmaxf(wind, 0.0f);
-        float f = 0.0f;
-        if (wind >= 3.0f && wind < 25.0f) f = wind >= 12.0f ? 1.0f : powf((wind - 3.0f) / 9.0f, 3.0f);
+        float f = 0.0f;  // cubic power curve: cut-in 3, rated 12, cut-out 25 m/s
+        if (wind >= 3.0f && wind < 25.0f) {
+          const float r = (wind - 3.0f) / 9.0f;
+          f = wind >= 12.0f ? 1.0f : r * r * r;
+        }
         v = peak * f;
       }
       tile[w][lane][j] = fminf(fmaxf(v, 0.0f), peak);
@@ -229,8 +248,11 @@ std::string launch_generate(float* caps, int64_t T, int64_t S, int64_t ld, int64
   const int64_t blocks = (warps + 7) / 8;
   const int64_t chunks = (S + kGenChunk - 1) / kGenChunk;
   if (chunks > 65535) return "trace too long for the generator (> 65535 chunks)";
+  // AR(1) coefficient of the 1 h cloud correlation, computed on the host in fp64 (libm exp) and
+  // rounded once: the host port (ora_generate_traces) derives it with the same expression
+  const float a_cloud = (float)std::exp(-(double)step_seconds / 3600.0);
   gen_kernel<<<dim3((unsigned)blocks, (unsigned)chunks), 256, 0, st>>>(caps, T, S, ld, first_id, step_seconds, kind,
-                                                                       peak, seed);
+                                                                       peak, seed, a_cloud);
   CS_CUDA_TRY(cudaGetLastError());
   return std::string();
 }

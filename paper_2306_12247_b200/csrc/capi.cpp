@@ -37,6 +37,8 @@ std::string launch_replay(const DevTables& v, int g, const double* caps, int64_t
                           int window_k, const int32_t* initial, double noise_pct, const uint32_t* keys,
                           const int32_t* key_len, int key_stride, unsigned long long seed_base, cs_replay_step* steps,
                           cs_replay_agg* agg, cudaStream_t st);
+std::string launch_sweep_totals(const cs_agg* agg, int64_t T, int rows, uint64_t* out, bool accumulate, int sms,
+                                cudaStream_t st);
 std::string launch_generate(float* caps, int64_t T, int64_t S, int64_t ld, int64_t first_id, int32_t step_seconds,
                             int32_t kind, float peak, uint64_t seed, cudaStream_t st);
 
@@ -349,9 +351,27 @@ int cs_eval(const cs_tables* tp, const cs_eval_args* a, void* stream) {
   if (rc) return rc;
   const Tables& t = *reinterpret_cast<const Tables*>(tp);
   if ((rc = check_eval_args(t, a))) return rc;
-  if (a->n_traces == 0) return CS_OK;
+  if (a->n_traces == 0) {  // no work, but an overwritten histogram must still read all-zero
+    if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST))
+      CS_CUDA_RET(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, reinterpret_cast<cudaStream_t>(stream)));
+    return CS_OK;
+  }
   std::string err = cs::launch_eval(t, d->view, a, dev, reinterpret_cast<cudaStream_t>(stream));
   if (!err.empty()) return fail(err.rfind("CUDA", 0) == 0 ? CS_E_CUDA : CS_E_INVALID, err);
+  return CS_OK;
+}
+
+int cs_sweep_totals(const cs_agg* agg_dev, int64_t n_traces, int32_t n_rows, uint64_t* totals_dev, uint32_t flags,
+                    void* stream) {
+  if (n_traces < 0 || n_rows < 1 || !totals_dev || (n_traces > 0 && !agg_dev))
+    return fail(CS_E_INVALID, "bad sweep arguments");
+  int dev = 0, sms = 148;
+  CS_CUDA_RET(cudaGetDevice(&dev));
+  CS_CUDA_RET(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::string err = cs::launch_sweep_totals(agg_dev, n_traces, n_rows, totals_dev,
+                                            (flags & CS_FLAG_ACCUMULATE_HIST) != 0, sms,
+                                            reinterpret_cast<cudaStream_t>(stream));
+  if (!err.empty()) return fail(CS_E_CUDA, err);
   return CS_OK;
 }
 
@@ -558,6 +578,8 @@ struct cs_engine {
   int device = 0;
   int cap_dtype = CS_CAP_F32;
   int64_t chunk = 0, smax = 0;
+  int64_t ld_dev = 0;  // row pitch (elements) of the device cap buffers
+  int64_t agg_rows = 0;  // grids x policies the aggregate buffers hold per trace
   cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
   void* dcaps[2] = {nullptr, nullptr};
   cs_agg* dagg[2] = {nullptr, nullptr};
@@ -585,6 +607,7 @@ int cs_engine_create(int32_t device, int64_t chunk_traces_max, int64_t n_steps_m
   const size_t esz = cap_dtype == CS_CAP_F32 ? 4 : 8;
   const int vec = cap_dtype == CS_CAP_F32 ? 4 : 2;
   const int64_t ld = (n_steps_max + vec - 1) / vec * vec;
+  e->ld_dev = ld;
   cudaError_t err = cudaSuccess;
   for (int i = 0; i < 2 && err == cudaSuccess; ++i) {
     err = cudaMalloc(&e->dcaps[i], (size_t)chunk_traces_max * ld * esz);
@@ -629,7 +652,9 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* tp, const void* caps_host
   if (!e || !tp || !caps_host || !agg_host) return fail(CS_E_INVALID, "null argument");
   const Tables& t = *reinterpret_cast<const Tables*>(tp);
   if (t.cap_dtype != e->cap_dtype) return fail(CS_E_INVALID, "engine and tables cap dtype differ");
+  if (n_traces < 0 || n_steps < 1) return fail(CS_E_INVALID, "bad sizes");
   if (n_steps > e->smax) return fail(CS_E_INVALID, "n_steps exceeds the engine's n_steps_max");
+  if (ld < n_steps) return fail(CS_E_INVALID, "ld must be >= n_steps");
   int prev = 0;
   CS_CUDA_RET(cudaGetDevice(&prev));
   CS_CUDA_RET(cudaSetDevice(e->device));
@@ -641,8 +666,12 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* tp, const void* caps_host
     cudaSetDevice(prev);
     return r;
   };
-  if (!e->dagg[0]) {
-    for (int i = 0; i < 2; ++i) CS_CUDA_RET(cudaMalloc(&e->dagg[i], agg_chunk * sizeof(cs_agg)));
+  if (e->agg_rows < M * 3) {  // sized for the tables of this call (more grids: grow)
+    for (int i = 0; i < 2; ++i) {
+      if (e->dagg[i]) cudaFree(e->dagg[i]), e->dagg[i] = nullptr;
+      CS_CUDA_RET(cudaMalloc(&e->dagg[i], agg_chunk * sizeof(cs_agg)));
+    }
+    e->agg_rows = M * 3;
   }
   if (e->hist_bins < t.U) {
     if (e->dhist) cudaFree(e->dhist);
@@ -655,7 +684,7 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* tp, const void* caps_host
   probe.caps = e->dcaps[0];
   probe.n_traces = std::min(n_traces, e->chunk);
   probe.n_steps = n_steps;
-  probe.ld = ld;
+  probe.ld = e->ld_dev;  // device rows keep the engine's pitch whatever the host pitch
   probe.step_seconds = step_seconds;
   probe.switch_penalty_s = switch_penalty_s;
   probe.flags = flags;
@@ -682,9 +711,16 @@ int cs_engine_eval_host(cs_engine* e, const cs_tables* tp, const void* caps_host
     const int64_t nt = std::min(e->chunk, n_traces - t0);
     // H2D into buffer b once the eval that last read it is done
     if (c >= 2) CS_CUDA_RET(cudaStreamWaitEvent(e->s_in, e->cmp_done[b], 0));
-    const size_t bytes = (size_t)nt * ld * esz;
-    CS_CUDA_RET(cudaMemcpyAsync(e->dcaps[b], reinterpret_cast<const unsigned char*>(caps_host) + (size_t)t0 * ld * esz,
-                                bytes, cudaMemcpyHostToDevice, e->s_in));
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(caps_host) + (size_t)t0 * ld * esz;
+    size_t bytes;
+    if (ld == e->ld_dev) {  // same pitch: one contiguous copy of whole rows
+      bytes = (size_t)nt * ld * esz;
+      CS_CUDA_RET(cudaMemcpyAsync(e->dcaps[b], src, bytes, cudaMemcpyHostToDevice, e->s_in));
+    } else {  // padded / strided host rows: copy the n_steps samples of each row into the engine's pitch
+      bytes = (size_t)nt * n_steps * esz;
+      CS_CUDA_RET(cudaMemcpy2DAsync(e->dcaps[b], (size_t)e->ld_dev * esz, src, (size_t)ld * esz, (size_t)n_steps * esz,
+                                    (size_t)nt, cudaMemcpyHostToDevice, e->s_in));
+    }
     h2d += (int64_t)bytes;
     CS_CUDA_RET(cudaEventRecord(e->in_done[b], e->s_in));
     // eval once the copy landed and the previous D2H of agg[b] drained

@@ -1166,7 +1166,8 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
           if (tiny ? wpg != wpc : wpg == 32) continue;  // tiny: one whole-CTA group per trace
           // ... of at most 512 threads when the trace is too short to split (C1, 1440 steps:
           // 14.7 us per step at 512 threads, 16.8 at 1024 — staging and barriers dominate)
-          if (tiny && a->n_steps < 4096 && threads > 512) continue;
+          // (unless the 3M + 1 per-group counters need the bigger CTA: > 170 grids)
+          if (tiny && a->n_steps < 4096 && threads > 512 && M * 3 + 1 <= 512) continue;
           if (force_wpg && wpg != force_wpg) continue;
           if (wpg * 32 < M * 3 + 1) continue;  // one thread per violation counter (+ the flag)
           const int gpc = wpc / wpg;
@@ -1362,6 +1363,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   g_last_plan.lut_entries = P.n_lut;
   g_last_plan.lut_shift = (int32_t)P.lv.shift1;
   g_last_plan.epilogue = P.bin_epi ? 2 : (P.seg_smem_bytes > 0 ? 1 : 0);
+  g_last_plan.redirect_uniform = (pl.uni && f32 && !pen && a->step_bins == nullptr) ? 1 : 0;
   return std::string();
 }
 

@@ -51,7 +51,6 @@ __device__ Sel select_comb(const DevTables& tb, int g, double x) {
   return s;
 }
 
-constexpr int kMaxWindow = 256;
 constexpr int kMaxKey = 8;
 
 __global__ void replay_kernel(const DevTables tb, int g, const double* __restrict__ caps, int64_t T, int64_t S,
@@ -93,8 +92,9 @@ __global__ void replay_kernel(const DevTables tb, int g, const double* __restric
   } else {
     cur = select_comb(tb, g, c[0]);  // step 0 (same element in both layouts)
   }
-  double hist[kMaxWindow];
-  int hlen = 0, hpos = 0;
+  // the proactive window (ControllerState.cap_history, a deque(maxlen=k) of the caps seen so far,
+  // controller.py:87,137) is the trace's own last min(k, i + 1) caps: read back from the cap row
+  // itself (L1/L2-resident), so any window_k works without per-thread history storage
   long long viol = 0, rec = 0;
   double th = 0.0, tl = 0.0;
   for (int64_t i = 0; i < S; ++i) {
@@ -113,17 +113,10 @@ __global__ void replay_kernel(const DevTables tb, int g, const double* __restric
       ++rec;
     }
     const uint16_t bin_r = cur.bin;
-    hist[hpos] = cap;
-    hpos = hpos + 1 == window_k ? 0 : hpos + 1;
-    if (hlen < window_k) ++hlen;
     if (mode == 1) {  // step_proactive (controller.py:125-142): predicted = fmean(history)
+      const int64_t hlen = i + 1 < (int64_t)window_k ? i + 1 : (int64_t)window_k;
       double sh = 0.0, sl = 0.0;
-      const int start = hlen < window_k ? 0 : hpos;
-      for (int q = 0; q < hlen; ++q) {
-        int idx = start + q;
-        if (idx >= window_k) idx -= window_k;
-        two_sum_acc(sh, sl, hist[idx]);
-      }
+      for (int64_t q = i + 1 - hlen; q <= i; ++q) two_sum_acc(sh, sl, c[q * cstride]);
       const double predicted = __ddiv_rn(__dadd_rn(sh, sl), (double)hlen);
       if (cur.entry >= 0 && predicted < cur.pw) {
         kb |= 2;
@@ -159,7 +152,7 @@ std::string launch_replay(const DevTables& v, int g, const double* caps, int64_t
                           int window_k, const int32_t* initial, double noise_pct, const uint32_t* keys,
                           const int32_t* key_len, int key_stride, unsigned long long seed_base, cs_replay_step* steps,
                           cs_replay_agg* agg, cudaStream_t st) {
-  if (window_k < 1 || window_k > kMaxWindow) return "window_k must be in [1, 256]";
+  if (window_k < 1) return "window_k must be >= 1";
   if (keys && (key_stride < 1 || key_stride > kMaxKey)) return "seed keys longer than 8 words are not supported";
   if (T <= 0) return std::string();
   const int threads = 128;

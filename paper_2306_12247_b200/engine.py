@@ -405,15 +405,20 @@ class EvalGraph:
     keeps (CS_FLAG_PREPARED). Inputs are read from ``caps`` at replay time, so refill it in place
     to evaluate new data; ``result`` holds the outputs of the latest replay."""
 
-    def __init__(self, tables: "Tables", caps, n_steps: int | None = None, **kw):
+    def __init__(self, tables: "Tables", caps, n_steps: int | None = None, *, sweep_totals: bool = False, **kw):
         torch = _torch()
+        from .shard import sweep_words
+
         self.tables = tables
         warm = tables.evaluate(caps, n_steps, **kw)  # outside capture: upload, plan memo, value tables
         torch.cuda.synchronize()
         self._ws = warm._ws
         self.graph = torch.cuda.CUDAGraph()
+        self.words = None  # sweep_totals: cs_sweep_totals of the replay's aggregates (same graph)
         with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
             self.result = tables.evaluate(caps, n_steps, _prepared_ws=self._ws, **kw)
+            if sweep_totals:
+                self.words = sweep_words(tables, self.result.agg)
         torch.cuda.synchronize()
 
     def replay(self) -> "EvalResult":
@@ -502,7 +507,14 @@ class HostEngine:
                  check_violations: bool = True, agg_out=None, hist_out=None):
         """caps_host: pinned (or pageable) host tensor [T, ld]. Returns (agg, hist, h2d, d2h)."""
         torch = _torch()
-        T, ld = caps_host.shape
+        dt = torch.float32 if self.tables.cap_dtype == "f32" else torch.float64
+        if caps_host.dtype != dt or caps_host.dim() != 2 or caps_host.is_cuda:
+            raise ValueError(f"caps_host must be a 2-D {dt} host tensor")
+        if caps_host.stride(1) != 1:
+            raise ValueError("caps_host rows must be contiguous")
+        T = caps_host.shape[0]
+        if not 1 <= int(n_steps) <= caps_host.shape[1]:
+            raise ValueError("n_steps must be in [1, caps_host.shape[1]]")
         M = self.tables.n_grids
         if agg_out is None:
             agg_out = torch.empty((T, M, 3, 6), dtype=torch.float64, pin_memory=True)
@@ -510,7 +522,8 @@ class HostEngine:
             hist_out = torch.empty(self.tables.n_union_bins, dtype=torch.int64, pin_memory=True)
         h2d, d2h = C.c_int64(), C.c_int64()
         N.check(N.lib().cs_engine_eval_host(
-            self._h, self.tables.handle, caps_host.data_ptr(), T, int(n_steps), caps_host.stride(0),
+            self._h, self.tables.handle, caps_host.data_ptr(), T, int(n_steps),
+            caps_host.stride(0) if T > 1 else caps_host.shape[1],
             int(step_seconds), float(switch_penalty_s), N.CS_FLAG_CHECK_VIOLATIONS if check_violations else 0,
             agg_out.data_ptr(), hist_out.data_ptr(), C.byref(h2d), C.byref(d2h)))
         return agg_out, hist_out, h2d.value, d2h.value

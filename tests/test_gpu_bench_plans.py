@@ -1,0 +1,157 @@
+"""GPU parity on the exact launch plans the benchmark runs (VERDICT r1 "parity holes").
+
+* C3's plan: the ten bench grids (5,000+ union thresholds), >= 4M timesteps, no per-step output,
+  enough traces that no trace is split -> the large-launch plan (finer LUT and segment tables
+  staged when they fit), multi-warp worker groups and (without a penalty) the warp-uniform
+  redirect kernel variant.
+* C2's plan: the ten grids over one or two long traces -> traces split across worker groups,
+  partial histograms and the per-(trace, grid) finalize kernel (gridDim.y = M).
+
+Each is compared with the pinned CPU oracle (oracle.simulate_batch / oracle.simulate, restating
+sim.py:104-188 and policy.py:136-148) on the bench's own generator output: idle counts,
+histograms and switch counts exact; sums within 1e-6 and >= 99.9 % bit-identical to fsum.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import REGIMES
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def torch(cuda_ok):
+    import torch as T
+
+    return T
+
+
+@pytest.fixture(scope="module")
+def cs(cuda_ok):
+    import paper_2306_12247_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def ten(cs):
+    import bench
+
+    return bench.make_grids("ten")
+
+
+def _oracle_grids(grids):
+    import bench
+
+    return bench.oracle_grids(grids)
+
+
+def _check_aggs(res, caps_np, grids, step, pen):
+    from oracle import oracle
+
+    avg, idle, en, _ = oracle.simulate_batch(_oracle_grids(grids), caps_np, step, pen, n_threads=16)
+    g_avg = res.avg_throughput_ips.cpu().numpy()
+    g_en = res.energy_proxy_wh.cpu().numpy()
+    assert np.array_equal(res.idle_steps.cpu().numpy(), idle)
+    assert np.all(res.violations.cpu().numpy() == 0)
+    assert np.allclose(g_avg, avg, rtol=REL_TOL, atol=0)
+    assert np.allclose(g_en, en, rtol=REL_TOL, atol=0)
+    exact = min(np.mean(g_avg == avg), np.mean(g_en == en))
+    assert exact > 0.999, f"only {exact:.4f} of sums bit-identical to fsum"
+
+
+def _check_switches(res, caps_np, grids, step, pen, traces):
+    from oracle import oracle
+
+    og = _oracle_grids(grids)
+    for t in traces:
+        for m in range(len(grids)):
+            for p, regime in enumerate(REGIMES):
+                r = oracle.simulate(og[m], caps_np[t].astype(np.float64), regime, step, pen)
+                want = int(np.sum(r.sel[1:] != r.sel[:-1])) if pen > 0 else 0
+                assert int(res.switches[t, m, p]) == want, (t, m, regime)
+
+
+def _check_hist_and_switches(res, tables, caps, S, step, pen):
+    """Histogram and switch counts of ``res`` against a per-step run (bins do not depend on the
+    penalty; with a penalty the ten grids' per-step launch would not fit shared memory)."""
+    ps = tables.evaluate(caps, S, step_seconds=step, per_step=True)
+    ub = ps.step_bins[:, :S].cpu().numpy().view(np.uint16).astype(np.int64)
+    hist = np.bincount(ub.ravel(), minlength=tables.n_union_bins)
+    if res.hist is not None:
+        assert np.array_equal(res.hist.cpu().numpy(), hist)
+    else:  # grids evaluated in chunks: per-grid config histograms
+        assert res.config_histograms() == tables.config_histograms(hist)
+    sw = res.switches.cpu().numpy()
+    for m in range(tables.n_grids):
+        gb = tables.grid_bins(m)
+        for p in range(3):
+            sel = gb.sel[p][gb.umap[ub]]
+            want = np.sum(sel[:, 1:] != sel[:, :-1], axis=1) if pen > 0 else np.zeros(sel.shape[0], np.int64)
+            assert np.array_equal(sw[:, m, p], want), (m, p)
+
+
+@pytest.mark.parametrize("kind", ["mixed", "iid"])
+@pytest.mark.parametrize("pen", [0.0, 10.0])
+def test_c3_plan_ten_grids_staged(cs, torch, ten, kind, pen):
+    T, S, step = 1536, 4096, 1  # 6.3M timesteps: the large-launch plan, one worker group per trace
+    caps = cs.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306)
+    torch.cuda.synchronize()
+    caps_np = caps[:, :S].cpu().numpy()
+    tables = cs.Tables.stage(ten, "f32")
+    res = tables.evaluate(caps, S, step_seconds=step, switch_penalty_s=pen, check_violations=True)
+    torch.cuda.synchronize()
+    plan = tables.last_plan()
+    assert plan["trace_segments"] == 1, plan
+    assert plan["warps_per_group"] > 1, plan
+    if pen == 0.0:
+        assert plan["redirect_uniform"] == 1, plan    # the UNI kernel C3 runs
+    _check_aggs(res, caps_np, ten, step, pen)
+    _check_hist_and_switches(res, tables, caps, S, step, pen)
+    _check_switches(res, caps_np, ten, step, pen, traces=(0, 1, T - 1))
+
+
+@pytest.mark.parametrize("pen", [0.0, 10.0])
+@pytest.mark.parametrize("T", [1, 2])
+def test_c2_plan_split_trace_finalize(cs, torch, ten, pen, T):
+    S, step = 300_007, 60  # one or two long traces: split across worker groups + per-grid finalize
+    caps = cs.generate_traces(T, S, step_seconds=step, kind="mixed", seed=2306)
+    torch.cuda.synchronize()
+    caps_np = caps[:, :S].cpu().numpy()
+    tables = cs.Tables.stage(ten, "f32")
+    res = tables.evaluate(caps, S, step_seconds=step, switch_penalty_s=pen)
+    torch.cuda.synchronize()
+    plan = tables.last_plan()
+    assert plan["trace_segments"] > 1, plan
+    assert tables.launch_count() == 3  # prep, eval, finalize (of the last grid chunk, if chunked)
+    _check_aggs(res, caps_np, ten, step, pen)
+    _check_hist_and_switches(res, tables, caps, S, step, pen)
+    _check_switches(res, caps_np, ten, step, pen, traces=range(T))
+    # the captured graph (what the bench replays) reproduces it
+    g = tables.capture(caps, S, step_seconds=step, switch_penalty_s=pen)
+    r = g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(r.agg, res.agg)
+    assert r.config_histograms() == res.config_histograms()
+
+
+def test_c4_plan_bin_epilogue_on_bench_traces(cs, torch):
+    """C4's plan (one grid, per-bin epilogue, staged finer LUT) on the bench generator's traces."""
+    import bench
+
+    grids = bench.make_grids("mobilenet")
+    T, S = 2048, 10080
+    caps = cs.generate_traces(T, S, step_seconds=60, kind="mixed", seed=2306)
+    torch.cuda.synchronize()
+    tables = cs.Tables.stage(grids, "f32")
+    res = tables.evaluate(caps, S, step_seconds=60)
+    torch.cuda.synchronize()
+    plan = tables.last_plan()
+    assert plan["epilogue"] == 2 and plan["trace_segments"] == 1, plan
+    _check_aggs(res, caps[:, :S].cpu().numpy(), grids, 60, 0.0)
+    _check_hist_and_switches(res, tables, caps, S, 60, 0.0)

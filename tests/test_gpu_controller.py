@@ -63,9 +63,13 @@ def test_replay_many_matches_oracle(cs):
     rng = np.random.default_rng(8)
     caps = np.clip(np.cumsum(rng.normal(0, 15, (40, 700)), axis=1) + 200, 0, 350)
     og = oracle_grid(g)
-    for mode, k, noise, seed in ((cs.REACTIVE, 1, 0.0, 0), (cs.proactive(4), 4, 3.0, 77)):
+    # windows beyond the old 256-sample history buffer: any window_k >= 1 works
+    for mode, k, noise, seed in ((cs.REACTIVE, 1, 0.0, 0), (cs.proactive(4), 4, 3.0, 77),
+                                 (cs.ControlMode(cs.REACTIVE.tag, window_k=300), 300, 2.0, 5),
+                                 (cs.proactive(300), 300, 1.0, 9), (cs.proactive(1000), 1000, 0.0, 1)):
         s = cs.replay_many(g, caps, mode, noise_pct=noise, seed=seed)
         for t in range(caps.shape[0]):
-            r = oracle.replay(og, caps[t], "proactive" if k > 1 else "reactive", k, -1, noise, seed + t)
+            proactive = mode.tag is not cs.REACTIVE.tag
+            r = oracle.replay(og, caps[t], "proactive" if proactive else "reactive", k, -1, noise, seed + t)
             assert s.violations[t] == r.violations and s.reconfigs[t] == r.reconfigs
             assert s.avg_throughput_ips[t] == pytest.approx(r.avg_throughput_ips, rel=1e-12, abs=0)

@@ -327,6 +327,22 @@ def test_generator_is_shard_invariant(cs, torch):
     assert float(a.std()) > 10.0
 
 
+@pytest.mark.parametrize("kind", ["solar", "wind", "mixed", "iid"])
+@pytest.mark.parametrize("step", [1, 60])
+def test_generator_matches_host_port(cs, torch, kind, step):
+    """The device generator and its host port (oracle.generate_traces) agree bit for bit, so the
+    bench's reference arm and CPU baseline run the reference algorithm on the same caps."""
+    from oracle import oracle
+
+    T, S = 70, 9001  # partial warps, three time chunks
+    dev = cs.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306, first_trace_id=5)
+    host = oracle.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306, first_trace_id=5)
+    torch.cuda.synchronize()
+    d = dev.cpu().numpy()
+    assert d.shape == host.shape
+    assert np.array_equal(d.view(np.uint32), host.view(np.uint32))
+
+
 def test_host_engine_matches_device_path(cs, torch):
     rng = np.random.default_rng(15)
     g = cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128))

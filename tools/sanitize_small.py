@@ -46,5 +46,15 @@ vals = np.clip(np.cumsum(np.random.default_rng(0).normal(0, 20, (8, 500)), axis=
 cs.replay_many(g, vals, cs.proactive(3), noise_pct=2.0, seed=1)
 trs = [cs.PowerTrace(f"t{i}", 60, datetime.datetime(2020, 1, 1), tuple(v.tolist())) for i, v in enumerate(vals)]
 cs.simulate_many([g], trs, kinds=[cs.sampling_policy(4, 1), cs.COMBINATION], switch_penalty_s=30.0)
+# C-ABI hardening cases (tests/test_gpu_abi_hardening.py): padded host rows copied 2-D into the
+# engine's pitch, an engine reused with more grids, a zero-trace launch
+host = torch.zeros((37, 1077), dtype=torch.float32).pin_memory()
+host[:, :1000] = caps[:37, :1000].cpu()
+eng = cs.HostEngine(cs.Tables.stage([g], "f32"), chunk_traces=8, n_steps_max=1000)
+eng.evaluate(host[:, :1000], 1000, step_seconds=60)
+eng.evaluate(host, 1000, step_seconds=60)
+eng.tables = t32
+eng.evaluate(host, 1000, step_seconds=60, switch_penalty_s=5.0)
+t32.evaluate(torch.zeros((0, 128), dtype=torch.float32, device="cuda"), 100, step_seconds=60)
 torch.cuda.synchronize()
 print("sanitize workload done")
