@@ -145,7 +145,7 @@ def test_c4_plan_bin_epilogue_on_bench_traces(cs, torch):
     import bench
 
     grids = bench.make_grids("mobilenet")
-    T, S = 2048, 10080
+    T, S = 10_000, 10080  # > 2 x (148 SMs x 32 one-warp groups): whole traces per group, as at C4
     caps = cs.generate_traces(T, S, step_seconds=60, kind="mixed", seed=2306)
     torch.cuda.synchronize()
     tables = cs.Tables.stage(grids, "f32")
