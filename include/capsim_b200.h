@@ -150,7 +150,8 @@ typedef struct {
   int32_t ctas, threads, warps_per_group, smem_bytes;
   int32_t trace_segments; /* > 1: long traces split across worker groups (+ finalize kernel) */
   int32_t lut_entries, lut_shift;
-  int32_t epilogue;       /* 0 segment tables from global, 1 staged segment tables, 2 per-bin */
+  int32_t epilogue;       /* 0 segment tables from global, 1 staged segment tables, 2 per-bin, 3/4 packed
+                             penalty counters, per touched bin (segment values from global / staged) */
   int32_t redirect_uniform; /* 1: the warp-uniform redirect kernel variant (redirect-heavy fp32 LUTs) */
 } cs_eval_plan;
 int cs_eval_last_plan(cs_eval_plan* out);

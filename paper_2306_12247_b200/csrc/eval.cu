@@ -117,6 +117,8 @@ struct EvalParams {
   // fp32 LUT constants of the redirect step derived on the host (kernel-parameter operands,
   // never rematerialised in the loop): shift and leaf mask one level down (s1 - 4)
   uint32_t lut_s2, lut_mask2;
+  // fp32 bits of the lowest union threshold: caps below it are union bin 0 (idle everywhere)
+  int32_t t0_bits;
   // shared-memory layout (bytes)
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
 };
@@ -482,6 +484,94 @@ __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uin
     for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
 }
 
+// PK epilogue (one grid, switching penalty): only the bins the trace touched (a few hundred of
+// C5's 2,038), each reading its three selection segments from the staged signature — no prefix
+// scan, no pass over every segment. Each warp compacts its share of nonzero bins into a queue in
+// the group scratch and processes them 32 at a time with every lane busy. Per policy p and bin u
+// with c steps of which s switched into u: thr += (c - s) x thr_k + s x thr_k (1 - pf),
+// energy += c x energy_k, k = seg_p(u), every value split {hi, lo} with split_q exactly as
+// prep_kernel does (sim.py:111, 119-122): the count x hi products and their sums are exact.
+// Re-zeroes both words of every touched bin.
+//   sraw[k] = {thr (0 when idle), energy} per selection segment, sq[4p..4p+3] = {Q_thr, 1/Q_thr,
+//   Q_energy, 1/Q_energy} of policy p
+//   (splitting on the fly beats loading prep_kernel's pre-split 48-B values through L1/L2:
+//   C5 2.65 vs 2.79 ms)
+template <typename GH>
+__device__ __forceinline__ void finish_trace_pk(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* hw,
+                                                const uint2* s_sig2, const uint32_t* vcnt, GH* ghist,
+                                                const double2* sraw, const double* sq, double* scratch, int gtid,
+                                                int gsize, int gid_local) {
+  const int U = P.tb.U;
+  const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
+  double a[3][4];
+  uint32_t idl[3] = {0u, 0u, 0u}, swc[3] = {0u, 0u, 0u};
+#pragma unroll
+  for (int p = 0; p < 3; ++p) a[p][0] = a[p][1] = a[p][2] = a[p][3] = 0.0;
+  auto bin = [&](int u) {
+    const uint32_t wa = h[u], wb = hw[u];
+    h[u] = 0u;
+    hw[u] = 0u;
+    const uint32_t c = wa & 0xFFFFu;
+    if (ghist) atomicAdd(&ghist[u], (GH)c);
+    const uint2 sg = s_sig2[u];
+    const uint32_t kk[3] = {sg.x >> 16, sg.y, sg.x & 0xFFFFu};
+    const uint32_t ss[3] = {wb >> 16, wa >> 16, wb & 0xFFFFu};
+    const double dc = (double)c;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const double2 r = sraw[kk[p]];
+      const double2 ve = split_q(r.y, sq[4 * p + 2], sq[4 * p + 3]);
+      a[p][2] = __fma_rn(dc, ve.x, a[p][2]);
+      a[p][3] = __fma_rn(dc, ve.y, a[p][3]);
+      swc[p] += ss[p];
+      if (u < P.fidle[p]) {
+        idl[p] += c;  // idle selection: zero throughput, switched or not
+      } else {
+        const double2 vt = split_q(r.x, sq[4 * p], sq[4 * p + 1]);
+        const double dn = (double)(c - ss[p]);
+        a[p][0] = __fma_rn(dn, vt.x, a[p][0]);
+        a[p][1] = __fma_rn(dn, vt.y, a[p][1]);
+        if (ss[p]) {
+          const double ds = (double)ss[p];
+          const double2 vp = split_q(__dmul_rn(r.x, P.omp), sq[4 * p], sq[4 * p + 1]);
+          a[p][0] = __fma_rn(ds, vp.x, a[p][0]);
+          a[p][1] = __fma_rn(ds, vp.y, a[p][1]);
+        }
+      }
+    }
+  };
+  // this warp's 32-bin chunks (interleaved across the group's warps: the touched bins cluster),
+  // compacted through a 64-entry u16 queue (128 B of scratch)
+  uint16_t* q = reinterpret_cast<uint16_t*>(scratch + wig * 24);
+  int n = 0;
+  for (int base = wig * 32; base < U; base += 32 * nw) {
+    const int u = base + lane;
+    const bool nz = u < U && h[u] != 0u;
+    const uint32_t m = __ballot_sync(0xffffffffu, nz);
+    if (nz) q[n + __popc(m & ((1u << lane) - 1u))] = (uint16_t)u;
+    n += __popc(m);
+    __syncwarp();
+    if (n >= 32) {
+      bin(q[lane]);
+      __syncwarp();
+      if (lane < n - 32) q[lane] = q[32 + lane];
+      n -= 32;
+      __syncwarp();
+    }
+  }
+  if (lane < n) bin(q[lane]);
+  __syncwarp();
+  double mine[3];
+  uint32_t ired[6];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    mine[p] = xreduce4(a[p], lane);
+    ired[p] = __reduce_add_sync(0xffffffffu, idl[p]);
+    ired[3 + p] = __reduce_add_sync(0xffffffffu, swc[p]);
+  }
+  store_aggs(P, t, 0, mine, ired, vcnt, scratch, lane, wig, nw, gid_local, gsize);
+}
+
 // Exact violation recount of a segment (slow path; only runs if the fast check fired).
 template <typename CapT>
 __device__ void recount_violations(const EvalParams& P, const uint32_t* s_lut, const CapT* row, int64_t s0,
@@ -551,7 +641,7 @@ constexpr uint32_t kStepZero = 0xFFFFFFFFu;  // "no previous step" (never a bin)
 
 // The hot loop over one segment [s0, s1e) of trace t. Returns true if a cap met a LUT leaf
 // that is not proven violation-free (the caller then recounts violations exactly).
-template <bool PEN, bool STEP, bool VIO, bool UNI>
+template <bool PEN, bool STEP, bool VIO, bool UNI, bool PK>
 __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* sw,
                                                 const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
                                                 int gsize) {
@@ -568,8 +658,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       for (int m = 0; m < M; ++m)
         count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], 0, 0, 0, sw_s, sw_dummy);
   };
-  // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
-  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4]) {
+  // union bins of one 16-B vector (4 caps) into b[] (LUT search only)
+  auto lut4 = [&](const uint4 raw, uint32_t (&b)[4]) {
     const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t e[4];
 #pragma unroll
@@ -615,6 +705,10 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], msk[k]);
     }
+  };
+  // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
+  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4]) {
+    lut4(raw, b);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
 #ifdef CS_DIAG_NO_ATOMS  // diagnostic build only: no histogram update (wrong aggregates)
@@ -650,7 +744,98 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     }
   };
 
-  if constexpr (PEN) {
+  // PK (one grid, switching penalty, < 2^16 steps per trace). Two words per union bin u: A[u] =
+  // [steps | switched steps of policy 1 << 16], W[u] = [switched of policy 2 | of policy 0 << 16]
+  // (16-bit fields cannot carry: a trace has < 2^16 steps). Per step three shared atomics, none
+  // predicated (ptxas turns predicated atomics into branches): the step count is ATOMS.POPC.INC —
+  // hardware-aggregated for equal addresses (idle night steps), where a register-operand add
+  // serialises 32-way (tools/microbench/mb_atoms.cu) — and the two switch increments go to the
+  // lane's own dummy slot when zero. The staged signature of bin u is {seg2 | seg0 << 16, seg1}
+  // (absolute selection-segment ids), so x = sig ^ sig_prev names the policies whose config
+  // changed (sim.py:119).
+  const uint2* s_sig2 = reinterpret_cast<const uint2*>(s_sig);
+  const uint32_t hA = (uint32_t)__cvta_generic_to_shared(h);
+  const uint32_t hW = PK ? (uint32_t)__cvta_generic_to_shared(sw) : 0u;
+  const uint32_t pk_dummy = hW + 4u * (uint32_t)(P.U4 + (gtid & 31));
+
+  auto pk_step = [&](uint32_t b, uint2 sc, uint2 sp) {
+    const uint32_t a = hA + 4u * b;
+    red_inc(a);
+    // 1 in each 16-bit half whose segment id changed (VIMNMX.U16x2)
+    uint32_t inc;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(inc) : "r"(sc.x ^ sp.x), "r"(0x00010001u));
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(inc ? hW + 4u * b : pk_dummy), "r"(inc) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(sc.y != sp.y ? a : pk_dummy) : "memory");
+  };
+  if constexpr (PK) {
+    // blocks of 128 vectors (512 steps) dealt round-robin to the group's warps: contiguous warp
+    // chunks (the PEN loop below) leave one warp the night and another the day, and the group
+    // then waits at its per-trace barriers. The cap before a block is re-read (one broadcast
+    // load per block) for the predecessor of the block's first step; inside a pass it comes by
+    // shuffle from lane - 1, and lane 0's from lane 31 of the previous pass.
+    const int lane = gtid & 31, nwg = gsize >> 5;
+    const int nblk = (nvf + 127) >> 7;
+    int ve = 0;
+    uint32_t carry = kStepZero;
+    auto pass = [&](const uint4 raw, int v) {
+      uint32_t b[4] = {0u, 0u, 0u, 0u};
+      const bool act = v < ve;
+      // idle fast path: every cap of the warp's pass below the lowest threshold (union bin 0:
+      // nothing feasible for any policy) and the step before it in bin 0 too, so no policy
+      // switches — 128 steps for bin 0 from one lane (night hours: ~2/3 of C5's mixed steps)
+      const int32_t t0 = P.t0_bits;
+      const bool low = act && (int32_t)raw.x < t0 && (int32_t)raw.y < t0 && (int32_t)raw.z < t0 && (int32_t)raw.w < t0;
+      if (__all_sync(0xffffffffu, low) && carry == 0u) {  // carry: warp-uniform
+        if (lane == 0) atomicAdd(h, 128u);
+        return;
+      }
+      if (act) lut4(raw, b);
+      const uint32_t left = __shfl_sync(0xffffffffu, b[3], (lane + 31) & 31);
+      uint32_t pb = lane == 0 ? carry : left;
+      carry = __shfl_sync(0xffffffffu, b[3], 31);
+      if (pb == kStepZero) pb = b[0];  // step 0 is never penalised (sim.py:119)
+      if (act) {
+        uint2 sg[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sg[k] = s_sig2[b[k]];
+        const uint2 sp = pb == b[0] ? sg[0] : s_sig2[pb];
+        pk_step(b[0], sg[0], sp);
+        pk_step(b[1], sg[1], sg[0]);
+        pk_step(b[2], sg[2], sg[1]);
+        pk_step(b[3], sg[3], sg[2]);
+      }
+    };
+    // the cap before each block is loaded one block ahead (its latency hides behind a block)
+    const uint32_t* crow = reinterpret_cast<const uint32_t*>(vrow);  // = row + s0
+    int blk = gtid >> 5;
+    uint32_t craw = 0u;
+    if (blk < nblk && s0 + 4 * (int64_t)(blk << 7) > 0) craw = __ldg(crow + 4 * (blk << 7) - 1);
+    for (; blk < nblk; blk += nwg) {
+      const int vb = blk << 7;
+      ve = min(nvf, vb + 128);
+      const int v = vb + lane;
+      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+      uint4 r0 = v < ve ? ldg_stream(vrow + (size_t)v * 16) : z;
+      uint4 r1 = v + 32 < ve ? ldg_stream(vrow + (size_t)(v + 32) * 16) : z;
+      uint4 r2 = v + 64 < ve ? ldg_stream(vrow + (size_t)(v + 64) * 16) : z;
+      uint4 r3 = v + 96 < ve ? ldg_stream(vrow + (size_t)(v + 96) * 16) : z;
+      carry = kStepZero;
+      if (s0 + 4 * (int64_t)vb > 0) {
+        uint32_t dummy = 0;
+        carry = L.bin(craw, dummy);
+      }
+      if (blk + nwg < nblk) craw = __ldg(crow + 4 * ((blk + nwg) << 7) - 1);
+#ifdef CS_PK_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+      for (int j = 0; j < 4; ++j) {
+        pass(r0, v + 32 * j);
+        r0 = r1, r1 = r2, r2 = r3;
+      }
+    }
+  } else if constexpr (PEN) {
     // Warp-contiguous chunks: each warp owns a run of vectors, lanes interleaved inside it, so the
     // cap before lane l's vector is lane l-1's last cap (a shuffle) and lane 0's is lane 31's of
     // the previous pass (carried in a register); only a warp's first vector reloads a cap.
@@ -720,6 +905,12 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     const int64_t gi = s0 + i;
     const uint32_t u = __ldg(row + gi);
     const uint32_t b = L.bin(u, flags);
+    if (PK) {
+      uint32_t dummy = 0;
+      const uint32_t pb = gi > 0 ? L.bin(__ldg(row + gi - 1), dummy) : b;
+      pk_step(b, s_sig2[b], s_sig2[pb]);
+      continue;
+    }
     atomicAdd(&h[b], 1u);
     if (PEN) {
       uint32_t dummy = 0;
@@ -843,7 +1034,7 @@ __device__ __forceinline__ bool run_segment_f64(const EvalParams& P, const Lut64
   return VIO && (flags & 0x4000u);
 }
 
-template <typename CapT, bool PEN, bool STEP, bool VIO, bool UNI = false>
+template <typename CapT, bool PEN, bool STEP, bool VIO, bool UNI = false, bool PK = false>
 __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ EvalParams P) {
   constexpr bool F32 = sizeof(CapT) == 4;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -858,7 +1049,17 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   if (!F32)
     for (int i = threadIdx.x; i < U - 1; i += blockDim.x) s_thr[i] = __ldg(P.lv.thr64 + i);
   uint64_t* s_sig = reinterpret_cast<uint64_t*>(smem + P.off_sig);
-  if (PEN) {
+  if (PK) {
+    // {seg2 | seg0 << 16, seg1}: absolute segment ids (see pk_step)
+    uint2* s2 = reinterpret_cast<uint2*>(s_sig);
+    const uint32_t f0 = (uint32_t)__ldg(tb.seg_off), f1 = (uint32_t)__ldg(tb.seg_off + 1),
+                   f2 = (uint32_t)__ldg(tb.seg_off + 2);
+    for (int i = threadIdx.x; i < U; i += blockDim.x) {
+      const uint64_t g = __ldg(tb.sig + i);
+      s2[i] = make_uint2((f2 + (uint32_t)((g >> 32) & 0xFFFFu)) | ((f0 + (uint32_t)(g & 0xFFFFu)) << 16),
+                         f1 + (uint32_t)((g >> 16) & 0xFFFFu));
+    }
+  } else if (PEN) {
     // signatures with each (grid, policy)'s first segment index folded in, so the 16-bit fields
     // are absolute switch-counter indices (the plan keeps NSEG <= 0xFFFF, so no field carries)
     for (int i = threadIdx.x; i < M * U; i += blockDim.x) {
@@ -886,7 +1087,16 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   int32_t* s_segidle = reinterpret_cast<int32_t*>(s_seghdr + ((P.NSEG + 3) & ~3));
   double2* s_segval = reinterpret_cast<double2*>(s_segidle + ((M * 3 + 3) & ~3));
   double2* s_binval = reinterpret_cast<double2*>(smem + P.off_seg);
-  if (!PEN && P.bin_epi) {
+  double2* s_pkraw = reinterpret_cast<double2*>(smem + P.off_seg);  // PK: {thr, energy} per segment
+  double* s_pkq = reinterpret_cast<double*>(s_pkraw + P.NSEG);         //     + the 3 policies' quanta
+  const double2* pk_raw = seg_staged ? s_pkraw : P.seg_raw;
+  const double* pk_q = seg_staged ? s_pkq : P.seg_q;
+  if (PK) {
+    if (seg_staged) {
+      for (int i = threadIdx.x; i < P.NSEG; i += blockDim.x) s_pkraw[i] = __ldg(P.seg_raw + i);
+      if (threadIdx.x < 12) s_pkq[threadIdx.x] = __ldg(P.seg_q + threadIdx.x);
+    }
+  } else if (!PEN && P.bin_epi) {
     for (int i = threadIdx.x; i < 6 * P.U4; i += blockDim.x) s_binval[i] = __ldg(P.bin_val + i);
   } else if (seg_staged) {
     const int NS = P.NSEG, NV = PEN ? 3 : 2;
@@ -906,7 +1116,9 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   double* scratch = reinterpret_cast<double*>(gbase + P.off_g_scr);
   const int U4 = P.U4;
   for (int u = gtid; u < U4; u += gsize) h[u] = 0u;
-  if (PEN)
+  if (PK)
+    for (int u = gtid; u < U4; u += gsize) sw[u] = 0u;
+  else if (PEN)
     for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
   if (gtid < M * 3) vcnt[gtid] = 0u;
   if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag (the plan keeps 3M < group size)
@@ -938,7 +1150,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     const int64_t s1e = min(P.S, s0 + P.seg_len);
     bool bad;
     if constexpr (F32)
-      bad = run_segment_f32<PEN, STEP, VIO, UNI>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+      bad = run_segment_f32<PEN, STEP, VIO, UNI, PK>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     else
       bad = run_segment_f64<PEN, STEP, VIO>(P, L64, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     if (VIO && bad) atomicOr(&vcnt[M * 3], 1u);
@@ -964,7 +1176,10 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
         }
       }
       uint32_t* gh = want_hist ? s_ghist : (uint32_t*)nullptr;
-      if (!PEN && P.bin_epi)
+      if (PK) {
+        finish_trace_pk(P, t, h, sw, reinterpret_cast<const uint2*>(s_sig), vcnt, gh, pk_raw, pk_q, scratch, gtid,
+                        gsize, gid_local);
+      } else if (!PEN && P.bin_epi)
         finish_trace_bins(P, t, h, vcnt, gh, s_binval, scratch, gtid, gsize, gid_local);
       else if (seg_staged)  // two instantiations so each reads its tables with a known address space
         finish_trace<PEN, false>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
@@ -1043,7 +1258,8 @@ thread_local bool g_timed = false;
 
 struct Plan {
   int threads, wpg, gpc, ctas;
-  bool uni = false;  // warp-uniform redirect variant (sub-tables > 5 % of the staged LUT's level-1 buckets)
+  bool uni = false;
+  bool pk = false;  // packed-penalty variant (PK)  // warp-uniform redirect variant (sub-tables > 5 % of the staged LUT's level-1 buckets)
   int32_t nseg;
   int64_t seg_len;
   size_t smem;
@@ -1058,13 +1274,16 @@ int sm_count(int dev) {
   return cache[dev];
 }
 
-template <typename CapT, bool PEN, bool STEP, bool VIO, bool UNI = false>
+template <typename CapT, bool PEN, bool STEP, bool VIO, bool UNI = false, bool PK = false>
 void* kptr() {
-  return (void*)eval_kernel<CapT, PEN, STEP, VIO, UNI>;
+  return (void*)eval_kernel<CapT, PEN, STEP, VIO, UNI, PK>;
 }
 
 // uni: the warp-uniform redirect variant (fp32, no penalty, no per-step output only)
-void* pick_kernel(bool f32, bool pen, bool step, bool vio, bool uni = false) {
+// pk: the packed-penalty variant (fp32, one grid, penalty, no per-step output, < 2^16 steps)
+void* pick_kernel(bool f32, bool pen, bool step, bool vio, bool uni = false, bool pk = false) {
+  if (pk && f32 && pen && !step)
+    return vio ? kptr<float, true, false, true, false, true>() : kptr<float, true, false, false, false, true>();
   if (uni && f32 && !pen && !step) return vio ? kptr<float, false, false, true, true>() : kptr<float, false, false, false, true>();
 #define CS_K(A, B, C) \
   if (pen == A && step == B && vio == C) return f32 ? kptr<float, A, B, C>() : kptr<double, A, B, C>();
@@ -1105,12 +1324,18 @@ int blocks_per_sm(void* fn, int dev, int threads, size_t smem) {
   return per_sm;
 }
 
-std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, Plan& pl) {
+std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args* a, int dev, Plan& pl,
+                      bool allow_pk = true) {
   const bool f32 = t.cap_dtype == CS_CAP_F32;
   const bool pen = a->switch_penalty_s > 0.0;
   const bool vio = (a->flags & CS_FLAG_CHECK_VIOLATIONS) != 0;
-  void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio);
   const int U = t.U, M = t.M;
+  // PK: 16-bit packed step / switched-step counters need < 2^16 steps per trace (whole traces per
+  // group; re-planned without it when the plan splits traces); CS_PLAN_NO_PK: tuning only
+  static const bool no_pk_env = std::getenv("CS_PLAN_NO_PK") != nullptr;
+  const bool pk = allow_pk && !no_pk_env && f32 && pen && M == 1 && a->step_bins == nullptr &&
+                  a->n_steps <= 0xFFFF && !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
+  void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio, false, pk);
   int smem_optin = 232448;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int nsm = sm_count(dev);
@@ -1131,11 +1356,14 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   const bool bin_epi = !pen && M == 1 && (double)a->n_traces * (double)a->n_steps >= (double)(1 << 22) &&
                        !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
   const size_t bin_bytes = (size_t)6 * U4 * 16;
-  const size_t seg_smem = bin_epi ? bin_bytes : a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
+  const size_t seg_smem = pk        ? a16((size_t)nsegs * 16 + 12 * 8)  // PK: {thr, energy} per segment + quanta
+                          : bin_epi ? bin_bytes
+                                    : a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
     size_t gb = a16((size_t)U4 * 4);
     *off_sw = gb;
-    gb += pen ? a16((size_t)(nsegs + 32) * 4) : 0;  // + 32 dummy slots (branch-free switch counting)
+    // PK: the second packed word per bin; else + 32 dummy slots (branch-free switch counting)
+    gb += pk ? a16((size_t)(U4 + 32) * 4) : pen ? a16((size_t)(nsegs + 32) * 4) : 0;
     *off_v = gb;
     gb += a16((size_t)(M * 3 + 1) * 4);
     *off_scr = gb;
@@ -1215,6 +1443,8 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   int64_t seg_len = (a->n_steps + nseg - 1) / nseg;
   seg_len = (seg_len + 127) / 128 * 128;
   nseg = (a->n_steps + seg_len - 1) / seg_len;
+  if (pk && nseg > 1) return make_plan(t, view, a, dev, pl, false);
+  pl.pk = pk;
   pl.nseg = (int32_t)nseg;
   pl.seg_len = seg_len;
   pl.ctas = (int)std::max<int64_t>(
@@ -1236,6 +1466,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     P.lut_mask2 = ((1u << s2) - 1u) & 0x3FFFu;
     pl.uni = f32 && (double)(P.n_lut - P.n_level1) / kSubFan > 0.05 * (double)P.n_level1;
   }
+  P.t0_bits = (f32 && !t.thresholds.empty()) ? (int32_t)(uint32_t)t.thresholds[0] : INT32_MIN;
   P.caps = a->caps;
   P.T = a->n_traces;
   P.S = a->n_steps;
@@ -1329,7 +1560,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
     P.part_vio = P.part_sw + (pen ? (size_t)a->n_traces * P.NSEG : 0);
     CS_CUDA_TRY(cudaMemsetAsync(w, 0, pl.ws_split, st));
   }
-  void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio, pl.uni);
+  void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio, pl.uni, pl.pk);
   CS_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   if (!g_ev0) {
     CS_CUDA_TRY(cudaEventCreate(&g_ev0));
@@ -1362,7 +1593,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   g_last_plan.trace_segments = pl.nseg;
   g_last_plan.lut_entries = P.n_lut;
   g_last_plan.lut_shift = (int32_t)P.lv.shift1;
-  g_last_plan.epilogue = P.bin_epi ? 2 : (P.seg_smem_bytes > 0 ? 1 : 0);
+  g_last_plan.epilogue = pl.pk ? (P.seg_smem_bytes > 0 ? 4 : 3) : P.bin_epi ? 2 : (P.seg_smem_bytes > 0 ? 1 : 0);
   g_last_plan.redirect_uniform = (pl.uni && f32 && !pen && a->step_bins == nullptr) ? 1 : 0;
   return std::string();
 }

@@ -155,3 +155,60 @@ def test_c4_plan_bin_epilogue_on_bench_traces(cs, torch):
     assert plan["epilogue"] == 2 and plan["trace_segments"] == 1, plan
     _check_aggs(res, caps[:, :S].cpu().numpy(), grids, 60, 0.0)
     _check_hist_and_switches(res, tables, caps, S, 60, 0.0)
+
+
+@pytest.mark.parametrize("kind", ["mixed", "iid"])
+@pytest.mark.parametrize("pen", [10.0, 60.0, 7.5])
+def test_c5_plan_packed_penalty(cs, torch, kind, pen):
+    """C5's plan: the fine 8x512 grid with a switching penalty -> the packed-penalty kernel (PK:
+    16|16-bit step / switched-step counters, policy 1's delta in registers, per-touched-bin
+    epilogue). Against the oracle and against the segment-counter path (segment_epilogue=True)."""
+    import bench
+
+    grids = bench.make_grids("fine")
+    T, S, step = 2048, 10080, 60  # 20.6M timesteps: whole traces per worker group
+    caps = cs.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306)
+    torch.cuda.synchronize()
+    caps_np = caps[:, :S].cpu().numpy()
+    tables = cs.Tables.stage(grids, "f32")
+    res = tables.evaluate(caps, S, step_seconds=step, switch_penalty_s=pen, check_violations=True)
+    torch.cuda.synchronize()
+    plan = tables.last_plan()
+    assert plan["epilogue"] in (3, 4) and plan["trace_segments"] == 1, plan
+    _check_aggs(res, caps_np, grids, step, pen)
+    _check_hist_and_switches(res, tables, caps, S, step, pen)
+    _check_switches(res, caps_np, grids, step, pen, traces=(0, 1, 7, T - 1))
+    old = tables.evaluate(caps, S, step_seconds=step, switch_penalty_s=pen, check_violations=True,
+                          segment_epilogue=True)
+    torch.cuda.synchronize()
+    assert tables.last_plan()["epilogue"] in (0, 1)
+    for f in ("idle_steps", "switches", "violations"):
+        assert torch.equal(getattr(res, f), getattr(old, f)), f
+    assert torch.equal(res.hist, old.hist)
+    assert torch.allclose(res.avg_throughput_ips, old.avg_throughput_ips, rtol=1e-12, atol=0)
+    assert torch.allclose(res.energy_proxy_wh, old.energy_proxy_wh, rtol=1e-12, atol=0)
+
+
+def test_pk_short_traces_and_tails(cs, torch):
+    """PK with ragged lengths (tails of < 4 caps, warp chunks that end mid-pass), a trace of one
+    step, and the plan falling back when a trace would be split (few traces)."""
+    import bench
+    from oracle import oracle
+
+    grids = bench.make_grids("fine")
+    og = bench.oracle_grids(grids)
+    tables = cs.Tables.stage(grids, "f32")
+    for T, S in ((4800, 1023), (4800, 5), (4800, 1), (3, 9000)):
+        caps = cs.generate_traces(T, S, step_seconds=60, kind="iid", seed=11)
+        torch.cuda.synchronize()
+        res = tables.evaluate(caps, S, step_seconds=60, switch_penalty_s=10.0)
+        torch.cuda.synchronize()
+        caps_np = caps[:, :S].cpu().numpy()
+        avg, idle, en, _ = oracle.simulate_batch(og, caps_np, 60, 10.0, n_threads=16)
+        assert np.array_equal(res.idle_steps.cpu().numpy(), idle), (T, S)
+        assert np.allclose(res.avg_throughput_ips.cpu().numpy(), avg, rtol=REL_TOL, atol=0), (T, S)
+        assert np.allclose(res.energy_proxy_wh.cpu().numpy(), en, rtol=REL_TOL, atol=0), (T, S)
+        for t in (0, T - 1):
+            for p, regime in enumerate(REGIMES):
+                r = oracle.simulate(og[0], caps_np[t].astype(np.float64), regime, 60, 10.0)
+                assert int(res.switches[t, 0, p]) == int(np.sum(r.sel[1:] != r.sel[:-1])), (T, S, t, regime)

@@ -31,6 +31,10 @@ tf = cs.Tables.stage([fine], "f32")
 fc = cs.generate_traces(4000, 256, step_seconds=60, kind="mixed", seed=6)
 tf.evaluate(fc, 256, step_seconds=60, switch_penalty_s=10.0)
 tf.evaluate(fc, 256, step_seconds=60)
+# packed-penalty kernel (PK): several 512-step blocks per trace, ragged tail, idle fast path
+fc2 = cs.generate_traces(2400, 1203, step_seconds=60, kind="mixed", seed=7)
+tf.evaluate(fc2, 1203, step_seconds=60, switch_penalty_s=10.0, check_violations=True)
+assert tf.last_plan()["epilogue"] in (3, 4), tf.last_plan()
 cs.Tables.stage([fine], "f64").evaluate(fc[:600].double(), 256, step_seconds=60, switch_penalty_s=10.0)
 # ten grids (5,055 union thresholds): the warp-uniform redirect variant
 import bench  # noqa: E402
