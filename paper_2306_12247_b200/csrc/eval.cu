@@ -29,6 +29,10 @@
 
 #include "cs_internal.h"
 
+#ifndef CS_PF_DIST
+#define CS_PF_DIST 0  // bulk L2 prefetch distance in batches (0: off)
+#endif
+
 namespace cs {
 namespace {
 
@@ -765,6 +769,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     uint32_t inc;
     asm("min.u16x2 %0, %1, %2;" : "=r"(inc) : "r"(sc.x ^ sp.x), "r"(0x00010001u));
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(inc ? hW + 4u * b : pk_dummy), "r"(inc) : "memory");
+    // (one register-operand add of 1 + (policy-1 switch << 16) instead of these two: C5 mixed
+    // 2.65 -> 3.02 ms, equal-address adds serialise; iid 4.62 -> 4.47 ms)
     asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(sc.y != sp.y ? a : pk_dummy) : "memory");
   };
   if constexpr (PK) {
@@ -886,9 +892,42 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       uint32_t b[4];
       bins4(raw, v, b);
     };
-    // each lane keeps 4 independent 128-bit loads in flight per pass
     int v = gtid;
+#ifdef CS_TC
+    if (!STEP) {
+      // time-clustered lanes: each warp instruction covers 32 CONSECUTIVE caps (4 coalesced 32-bit
+      // loads per 128-cap window: lane l takes caps l, l + 32, l + 64, l + 96), so slowly varying
+      // caps hit fewer distinct LUT entries / histogram bins per instruction
+      const int lane = gtid & 31;
+      const uint32_t* crow = reinterpret_cast<const uint32_t*>(vrow);
+      for (; v + 3 * gsize < nvf; v += 4 * gsize) {
+        uint4 r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t* w = crow + 4 * (size_t)(v - lane + i * gsize) + lane;
+          r[i].x = __ldg(w);
+          r[i].y = __ldg(w + 32);
+          r[i].z = __ldg(w + 64);
+          r[i].w = __ldg(w + 96);
+        }
+        vec4(r[0], v);
+        vec4(r[1], v + gsize);
+        vec4(r[2], v + 2 * gsize);
+        vec4(r[3], v + 3 * gsize);
+      }
+    }
+#endif
+    // each lane keeps 4 independent 128-bit loads in flight per pass
     for (; v + 3 * gsize < nvf; v += 4 * gsize) {
+#if CS_PF_DIST > 0
+      // bulk L2 prefetch (TMA unit, no registers) of this warp's 2-KB slice of the group's batch
+      // CS_PF_DIST batches ahead, so the loads below hit L2 instead of waiting on DRAM
+      if ((gtid & 31) == 0) {
+        const int64_t pv = (int64_t)(v - gtid) + (int64_t)CS_PF_DIST * 4 * gsize + (int64_t)(gtid >> 5) * 128;
+        if (pv + 128 <= nvf)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], 2048;" ::"l"(vrow + pv * 16) : "memory");
+      }
+#endif
       const uint4 r0 = ldg_stream(vrow + (size_t)v * 16);
       const uint4 r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16);
       const uint4 r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16);

@@ -104,6 +104,13 @@ def _check_cap(cap_w: float) -> None:
         raise ValueError(f"cap_w must be >= 0, got {cap_w}")
 
 
+def _regime_index(kind: PolicyKind) -> int:
+    """_regime_entries (policy.py:100-107): batching and multi-tenant slice the grid, every other
+    kind (combination, sampling) takes all entries — so a PolicyIndex of a sampling kind is the
+    combination index (policy.py:118-134)."""
+    return _POLICY_INDEX.get(kind.tag, _POLICY_INDEX[PolicyTag.COMBINATION])
+
+
 def _exhaustive(kind: PolicyKind) -> int:
     if kind.tag is PolicyTag.SAMPLING:
         raise ValueError("sampling is not an exhaustive policy; use select_sampling")
@@ -135,7 +142,7 @@ class PolicyIndex:
 
         self.grid = grid
         self.kind = kind
-        self._p = _exhaustive(kind)
+        self._p = _regime_index(kind)
         self._tables = Tables.for_grid(grid, "f64", batching_mtl=batching_mtl, multi_tenant_bs=multi_tenant_bs)
         gb = self._tables.grid_bins(0)
         self._decode = selections_for_bins(grid, gb.sel[self._p], gb.count[self._p])
@@ -217,7 +224,7 @@ def feasible_set(grid: ProfileGrid, kind: PolicyKind, cap_w: float, *, batching_
     from .engine import Tables
 
     _check_cap(cap_w)
-    p = 2 if kind.tag is PolicyTag.SAMPLING else _POLICY_INDEX[kind.tag]
+    p = _regime_index(kind)
     from . import _native as N
 
     tables = Tables.for_grid(grid, "f64", batching_mtl=batching_mtl, multi_tenant_bs=multi_tenant_bs)

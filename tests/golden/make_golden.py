@@ -152,7 +152,16 @@ def policy_golden() -> dict:
     for label, kind in KINDS.items():
         quirks[label] = {"inf": sel_doc(select_config(g1, kind, math.inf)),
                          "nan": sel_doc(select_config(g1, kind, math.nan))}
-    return {"source": "capsim 0.1.0 reference, policy.py:110-188", "cases": docs, "g1_quirks": quirks}
+    # PolicyIndex of a sampling kind: _regime_entries gives it every entry (policy.py:100-107), so
+    # it answers like the combination index (it is select_config that rejects sampling kinds)
+    from capsim.policy import sampling_policy
+
+    sampling_index = {}
+    for name, grid, caps, _, _ in (cases[0], cases[-1]):
+        idx = PolicyIndex(grid, sampling_policy(4, 2))
+        sampling_index[name] = [sel_doc(idx.select(c)) for c in caps]
+    return {"source": "capsim 0.1.0 reference, policy.py:110-188", "cases": docs, "g1_quirks": quirks,
+            "sampling_index": sampling_index}
 
 
 def steps_digest(report) -> dict:

@@ -70,6 +70,19 @@ def test_select_config_golden(cs):
                 assert sorted([c.mtl, c.bs] for c in fs) == want
 
 
+def test_policy_index_of_sampling_kind_is_combination(cs):
+    """PolicyIndex(grid, sampling_policy(m, r)) indexes every entry like the combination regime
+    (reference policy.py:100-107, 118-134); only select_config rejects sampling kinds."""
+    doc = golden("policy_golden.json")
+    by_name = {c["name"]: c for c in doc["cases"]}
+    for name, want in doc["sampling_index"].items():
+        case = by_name[name]
+        grid = grid_from_doc(case["grid"])
+        idx = cs.PolicyIndex(grid, cs.sampling_policy(4, 2))
+        assert [sel_doc(s) for s in idx.select_many(case["caps"])] == want, name
+        assert want == case["select"]["combination"], name
+
+
 def test_select_config_quirks(cs):
     doc = golden("policy_golden.json")
     g1 = grid_from_doc(doc["cases"][0]["grid"])
