@@ -213,7 +213,8 @@ def traffic_of(config: str, kind: str, dtype: str):
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
-    return json.loads(p.read_text()).get(f"{config}:{kind}:{dtype}")
+    d = json.loads(p.read_text())
+    return d.get(f"{config}:{kind}:{dtype}") or (d.get(f"{config}:{kind}") if dtype == "f32" else None)
 
 
 def cpu_baseline(grids, caps_host, cfg, budget_s: float, threads: int | None = None):

@@ -125,6 +125,7 @@ struct EvalParams {
   int32_t t0_bits;
   // shared-memory layout (bytes)
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
+  int32_t off_pkq, off_g_edge;  // PK: the 3 policies' quanta (CTA), block edges (per group)
 };
 
 namespace {
@@ -488,94 +489,6 @@ __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uin
     for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
 }
 
-// PK epilogue (one grid, switching penalty): only the bins the trace touched (a few hundred of
-// C5's 2,038), each reading its three selection segments from the staged signature — no prefix
-// scan, no pass over every segment. Each warp compacts its share of nonzero bins into a queue in
-// the group scratch and processes them 32 at a time with every lane busy. Per policy p and bin u
-// with c steps of which s switched into u: thr += (c - s) x thr_k + s x thr_k (1 - pf),
-// energy += c x energy_k, k = seg_p(u), every value split {hi, lo} with split_q exactly as
-// prep_kernel does (sim.py:111, 119-122): the count x hi products and their sums are exact.
-// Re-zeroes both words of every touched bin.
-//   sraw[k] = {thr (0 when idle), energy} per selection segment, sq[4p..4p+3] = {Q_thr, 1/Q_thr,
-//   Q_energy, 1/Q_energy} of policy p
-//   (splitting on the fly beats loading prep_kernel's pre-split 48-B values through L1/L2:
-//   C5 2.65 vs 2.79 ms)
-template <typename GH>
-__device__ __forceinline__ void finish_trace_pk(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* hw,
-                                                const uint2* s_sig2, const uint32_t* vcnt, GH* ghist,
-                                                const double2* sraw, const double* sq, double* scratch, int gtid,
-                                                int gsize, int gid_local) {
-  const int U = P.tb.U;
-  const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
-  double a[3][4];
-  uint32_t idl[3] = {0u, 0u, 0u}, swc[3] = {0u, 0u, 0u};
-#pragma unroll
-  for (int p = 0; p < 3; ++p) a[p][0] = a[p][1] = a[p][2] = a[p][3] = 0.0;
-  auto bin = [&](int u) {
-    const uint32_t wa = h[u], wb = hw[u];
-    h[u] = 0u;
-    hw[u] = 0u;
-    const uint32_t c = wa & 0xFFFFu;
-    if (ghist) atomicAdd(&ghist[u], (GH)c);
-    const uint2 sg = s_sig2[u];
-    const uint32_t kk[3] = {sg.x >> 16, sg.y, sg.x & 0xFFFFu};
-    const uint32_t ss[3] = {wb >> 16, wa >> 16, wb & 0xFFFFu};
-    const double dc = (double)c;
-#pragma unroll
-    for (int p = 0; p < 3; ++p) {
-      const double2 r = sraw[kk[p]];
-      const double2 ve = split_q(r.y, sq[4 * p + 2], sq[4 * p + 3]);
-      a[p][2] = __fma_rn(dc, ve.x, a[p][2]);
-      a[p][3] = __fma_rn(dc, ve.y, a[p][3]);
-      swc[p] += ss[p];
-      if (u < P.fidle[p]) {
-        idl[p] += c;  // idle selection: zero throughput, switched or not
-      } else {
-        const double2 vt = split_q(r.x, sq[4 * p], sq[4 * p + 1]);
-        const double dn = (double)(c - ss[p]);
-        a[p][0] = __fma_rn(dn, vt.x, a[p][0]);
-        a[p][1] = __fma_rn(dn, vt.y, a[p][1]);
-        if (ss[p]) {
-          const double ds = (double)ss[p];
-          const double2 vp = split_q(__dmul_rn(r.x, P.omp), sq[4 * p], sq[4 * p + 1]);
-          a[p][0] = __fma_rn(ds, vp.x, a[p][0]);
-          a[p][1] = __fma_rn(ds, vp.y, a[p][1]);
-        }
-      }
-    }
-  };
-  // this warp's 32-bin chunks (interleaved across the group's warps: the touched bins cluster),
-  // compacted through a 64-entry u16 queue (128 B of scratch)
-  uint16_t* q = reinterpret_cast<uint16_t*>(scratch + wig * 24);
-  int n = 0;
-  for (int base = wig * 32; base < U; base += 32 * nw) {
-    const int u = base + lane;
-    const bool nz = u < U && h[u] != 0u;
-    const uint32_t m = __ballot_sync(0xffffffffu, nz);
-    if (nz) q[n + __popc(m & ((1u << lane) - 1u))] = (uint16_t)u;
-    n += __popc(m);
-    __syncwarp();
-    if (n >= 32) {
-      bin(q[lane]);
-      __syncwarp();
-      if (lane < n - 32) q[lane] = q[32 + lane];
-      n -= 32;
-      __syncwarp();
-    }
-  }
-  if (lane < n) bin(q[lane]);
-  __syncwarp();
-  double mine[3];
-  uint32_t ired[6];
-#pragma unroll
-  for (int p = 0; p < 3; ++p) {
-    mine[p] = xreduce4(a[p], lane);
-    ired[p] = __reduce_add_sync(0xffffffffu, idl[p]);
-    ired[3 + p] = __reduce_add_sync(0xffffffffu, swc[p]);
-  }
-  store_aggs(P, t, 0, mine, ired, vcnt, scratch, lane, wig, nw, gid_local, gsize);
-}
-
 // Exact violation recount of a segment (slow path; only runs if the fast check fired).
 template <typename CapT>
 __device__ void recount_violations(const EvalParams& P, const uint32_t* s_lut, const CapT* row, int64_t s0,
@@ -645,7 +558,7 @@ constexpr uint32_t kStepZero = 0xFFFFFFFFu;  // "no previous step" (never a bin)
 
 // The hot loop over one segment [s0, s1e) of trace t. Returns true if a cap met a LUT leaf
 // that is not proven violation-free (the caller then recounts violations exactly).
-template <bool PEN, bool STEP, bool VIO, bool UNI, bool PK>
+template <bool PEN, bool STEP, bool VIO, bool UNI>
 __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* sw,
                                                 const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
                                                 int gsize) {
@@ -748,100 +661,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     }
   };
 
-  // PK (one grid, switching penalty, < 2^16 steps per trace). Two words per union bin u: A[u] =
-  // [steps | switched steps of policy 1 << 16], W[u] = [switched of policy 2 | of policy 0 << 16]
-  // (16-bit fields cannot carry: a trace has < 2^16 steps). Per step three shared atomics, none
-  // predicated (ptxas turns predicated atomics into branches): the step count is ATOMS.POPC.INC —
-  // hardware-aggregated for equal addresses (idle night steps), where a register-operand add
-  // serialises 32-way (tools/microbench/mb_atoms.cu) — and the two switch increments go to the
-  // lane's own dummy slot when zero. The staged signature of bin u is {seg2 | seg0 << 16, seg1}
-  // (absolute selection-segment ids), so x = sig ^ sig_prev names the policies whose config
-  // changed (sim.py:119).
-  const uint2* s_sig2 = reinterpret_cast<const uint2*>(s_sig);
-  const uint32_t hA = (uint32_t)__cvta_generic_to_shared(h);
-  const uint32_t hW = PK ? (uint32_t)__cvta_generic_to_shared(sw) : 0u;
-  const uint32_t pk_dummy = hW + 4u * (uint32_t)(P.U4 + (gtid & 31));
-
-  auto pk_step = [&](uint32_t b, uint2 sc, uint2 sp) {
-    const uint32_t a = hA + 4u * b;
-    red_inc(a);
-    // 1 in each 16-bit half whose segment id changed (VIMNMX.U16x2)
-    uint32_t inc;
-    asm("min.u16x2 %0, %1, %2;" : "=r"(inc) : "r"(sc.x ^ sp.x), "r"(0x00010001u));
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(inc ? hW + 4u * b : pk_dummy), "r"(inc) : "memory");
-    // (one register-operand add of 1 + (policy-1 switch << 16) instead of these two: C5 mixed
-    // 2.65 -> 3.02 ms, equal-address adds serialise; iid 4.62 -> 4.47 ms)
-    asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(sc.y != sp.y ? a : pk_dummy) : "memory");
-  };
-  if constexpr (PK) {
-    // blocks of 128 vectors (512 steps) dealt round-robin to the group's warps: contiguous warp
-    // chunks (the PEN loop below) leave one warp the night and another the day, and the group
-    // then waits at its per-trace barriers. The cap before a block is re-read (one broadcast
-    // load per block) for the predecessor of the block's first step; inside a pass it comes by
-    // shuffle from lane - 1, and lane 0's from lane 31 of the previous pass.
-    const int lane = gtid & 31, nwg = gsize >> 5;
-    const int nblk = (nvf + 127) >> 7;
-    int ve = 0;
-    uint32_t carry = kStepZero;
-    auto pass = [&](const uint4 raw, int v) {
-      uint32_t b[4] = {0u, 0u, 0u, 0u};
-      const bool act = v < ve;
-      // idle fast path: every cap of the warp's pass below the lowest threshold (union bin 0:
-      // nothing feasible for any policy) and the step before it in bin 0 too, so no policy
-      // switches — 128 steps for bin 0 from one lane (night hours: ~2/3 of C5's mixed steps)
-      const int32_t t0 = P.t0_bits;
-      const bool low = act && (int32_t)raw.x < t0 && (int32_t)raw.y < t0 && (int32_t)raw.z < t0 && (int32_t)raw.w < t0;
-      if (__all_sync(0xffffffffu, low) && carry == 0u) {  // carry: warp-uniform
-        if (lane == 0) atomicAdd(h, 128u);
-        return;
-      }
-      if (act) lut4(raw, b);
-      const uint32_t left = __shfl_sync(0xffffffffu, b[3], (lane + 31) & 31);
-      uint32_t pb = lane == 0 ? carry : left;
-      carry = __shfl_sync(0xffffffffu, b[3], 31);
-      if (pb == kStepZero) pb = b[0];  // step 0 is never penalised (sim.py:119)
-      if (act) {
-        uint2 sg[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sg[k] = s_sig2[b[k]];
-        const uint2 sp = pb == b[0] ? sg[0] : s_sig2[pb];
-        pk_step(b[0], sg[0], sp);
-        pk_step(b[1], sg[1], sg[0]);
-        pk_step(b[2], sg[2], sg[1]);
-        pk_step(b[3], sg[3], sg[2]);
-      }
-    };
-    // the cap before each block is loaded one block ahead (its latency hides behind a block)
-    const uint32_t* crow = reinterpret_cast<const uint32_t*>(vrow);  // = row + s0
-    int blk = gtid >> 5;
-    uint32_t craw = 0u;
-    if (blk < nblk && s0 + 4 * (int64_t)(blk << 7) > 0) craw = __ldg(crow + 4 * (blk << 7) - 1);
-    for (; blk < nblk; blk += nwg) {
-      const int vb = blk << 7;
-      ve = min(nvf, vb + 128);
-      const int v = vb + lane;
-      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-      uint4 r0 = v < ve ? ldg_stream(vrow + (size_t)v * 16) : z;
-      uint4 r1 = v + 32 < ve ? ldg_stream(vrow + (size_t)(v + 32) * 16) : z;
-      uint4 r2 = v + 64 < ve ? ldg_stream(vrow + (size_t)(v + 64) * 16) : z;
-      uint4 r3 = v + 96 < ve ? ldg_stream(vrow + (size_t)(v + 96) * 16) : z;
-      carry = kStepZero;
-      if (s0 + 4 * (int64_t)vb > 0) {
-        uint32_t dummy = 0;
-        carry = L.bin(craw, dummy);
-      }
-      if (blk + nwg < nblk) craw = __ldg(crow + 4 * ((blk + nwg) << 7) - 1);
-#ifdef CS_PK_UNROLL
-#pragma unroll
-#else
-#pragma unroll 1
-#endif
-      for (int j = 0; j < 4; ++j) {
-        pass(r0, v + 32 * j);
-        r0 = r1, r1 = r2, r2 = r3;
-      }
-    }
-  } else if constexpr (PEN) {
+  if constexpr (PEN) {
     // Warp-contiguous chunks: each warp owns a run of vectors, lanes interleaved inside it, so the
     // cap before lane l's vector is lane l-1's last cap (a shuffle) and lane 0's is lane 31's of
     // the previous pass (carried in a register); only a warp's first vector reloads a cap.
@@ -917,6 +737,28 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       }
     }
 #endif
+#ifdef CS_ROLL
+    // rolling pipeline: each vector's register is reloaded with the next batch's vector as soon
+    // as it is consumed, so loads stay in flight while the batch computes
+    if (v + 3 * gsize < nvf) {
+      uint4 r0 = ldg_stream(vrow + (size_t)v * 16), r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16),
+            r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16), r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
+      for (;;) {
+        const int vn = v + 4 * gsize;
+        const bool more = vn + 3 * gsize < nvf;
+        vec4(r0, v);
+        if (more) r0 = ldg_stream(vrow + (size_t)vn * 16);
+        vec4(r1, v + gsize);
+        if (more) r1 = ldg_stream(vrow + (size_t)(vn + gsize) * 16);
+        vec4(r2, v + 2 * gsize);
+        if (more) r2 = ldg_stream(vrow + (size_t)(vn + 2 * gsize) * 16);
+        vec4(r3, v + 3 * gsize);
+        if (more) r3 = ldg_stream(vrow + (size_t)(vn + 3 * gsize) * 16);
+        v = vn;
+        if (!more) break;
+      }
+    }
+#endif
     // each lane keeps 4 independent 128-bit loads in flight per pass
     for (; v + 3 * gsize < nvf; v += 4 * gsize) {
 #if CS_PF_DIST > 0
@@ -944,12 +786,6 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     const int64_t gi = s0 + i;
     const uint32_t u = __ldg(row + gi);
     const uint32_t b = L.bin(u, flags);
-    if (PK) {
-      uint32_t dummy = 0;
-      const uint32_t pb = gi > 0 ? L.bin(__ldg(row + gi - 1), dummy) : b;
-      pk_step(b, s_sig2[b], s_sig2[pb]);
-      continue;
-    }
     atomicAdd(&h[b], 1u);
     if (PEN) {
       uint32_t dummy = 0;
@@ -958,6 +794,309 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     if (STEP) P.step_bins[t * P.ld_bins + gi] = (uint16_t)b;
   }
   return VIO && (flags & 1u);
+}
+
+// ---------------------------------------------------------------------------------------------
+// PK: one grid, switching penalty, whole traces of < 2^16 steps (C5's shape). Per worker group:
+//   h[u]  = A word: steps in union bin u | switched steps of policy 1 << 16
+//   hw[u] = W word: switched steps of policy 2 | of policy 0 << 16, + 32 per-lane dummy slots
+//   edges[i] = first bin | last bin << 16 of block i (kPkBlkVec vectors, dealt round-robin)
+// 16-bit fields cannot carry: a trace has < 2^16 steps (the plan also counts the fill below).
+// ---------------------------------------------------------------------------------------------
+constexpr int kPkBlkVec = 64;  // vectors (4 caps each) per block: two 32-lane passes
+
+// bins of 4 caps (no redirect-uniform variant), ORing the leaves into flags
+__device__ __forceinline__ void lut4_f32(const Lut32& L, const uint4 raw, uint32_t (&b)[4], uint32_t& flags) {
+  const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t e[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) e[k] = L.entry(u[k]);
+  const uint32_t any = e[0] | e[1] | e[2] | e[3];
+  if ((int32_t)any >= 0) {
+    flags |= any;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
+  } else {
+    uint32_t msk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      msk[k] = L.mask1;
+      if (e[k] >= kRedirect32) {
+        msk[k] = L.mask2;
+        e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> L.s2) & 15u)];
+      }
+    }
+    if (e[0] >= kRedirect32 || e[1] >= kRedirect32 || e[2] >= kRedirect32 || e[3] >= kRedirect32) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        while (e[k] >= kRedirect32) {
+          const uint32_t sh = e[k] & 31u;
+          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh) & 15u)];
+          msk[k] = ((1u << sh) - 1u) & 0x3FFFu;
+        }
+    }
+    flags |= e[0] | e[1] | e[2] | e[3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], msk[k]);
+  }
+}
+
+// One step of bin b whose segments are sc after sp (sim.py:119: a policy whose config changed pays
+// the penalty). Three shared atomics, none predicated (ptxas turns predicated atomics into
+// branches): the step count is ATOMS.POPC.INC — hardware-aggregated for equal addresses, where a
+// register-operand add serialises (tools/microbench/mb_atoms.cu) — and the two switch increments
+// go to the lane's own dummy slot when zero. sig = {seg2 | seg0 << 16, seg1} (absolute segment
+// ids), so sc ^ sp names the policies whose config changed.
+__device__ __forceinline__ void pk_count(uint32_t hA, uint32_t hW, uint32_t dummy, uint32_t b, uint2 sc, uint2 sp) {
+  const uint32_t a = hA + 4u * b;
+  red_inc(a);
+  uint32_t inc;  // 1 in each 16-bit half whose segment id changed (VIMNMX.U16x2)
+  asm("min.u16x2 %0, %1, %2;" : "=r"(inc) : "r"(sc.x ^ sp.x), "r"(0x00010001u));
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(inc ? hW + 4u * b : dummy), "r"(inc) : "memory");
+  asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(sc.y != sp.y ? a : dummy) : "memory");
+}
+
+// Main loop of one whole trace (s0 = 0). Blocks of kPkBlkVec vectors are dealt round-robin to the
+// group's warps (a warp's contiguous share could be all night while another's is all day, and the
+// group waits at its per-trace barrier). Inside a block the cap before lane l's vector is lane
+// l-1's last (a shuffle) and lane 0's comes from lane 31 of the previous pass; a block's first
+// step is counted unswitched and its (first, last) bins go to edges[] — pk_finish adds the
+// switches across block boundaries. Each lane keeps the next block's loads in flight under the
+// current block (two unrolled passes, no register rotation). Vectors past the end of the trace
+// replicate its last full vector's last cap (no predication in the passes); their steps, all in
+// that cap's bin, are subtracted once at the end. Returns true if a cap met an unproven leaf.
+__device__ __forceinline__ bool pk_main(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* hw,
+                                        uint32_t* edges, const uint2* s_sig2, int64_t t, int gtid, int gsize) {
+  const int n = (int)P.S;
+  const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
+  const uint4* vrow = reinterpret_cast<const uint4*>(row);
+  const int nvf = n >> 2;
+  const int lane = gtid & 31, wig = gtid >> 5, nwg = gsize >> 5;
+  const int nblk = (nvf + kPkBlkVec - 1) / kPkBlkVec;
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t hA = (uint32_t)__cvta_generic_to_shared(h), hW = (uint32_t)__cvta_generic_to_shared(hw);
+  const uint32_t dummy = hW + 4u * (uint32_t)(P.U4 + lane);
+  const int32_t t0 = P.t0_bits;
+  uint32_t flags = 0;
+  auto ldv = [&](int v) -> uint4 {
+    const uint4 r = ldg_stream(vrow + min(v, nvf - 1));
+    return v < nvf ? r : make_uint4(r.w, r.w, r.w, r.w);
+  };
+  uint32_t carry = 0u, bfirst = 0u;
+  auto pass = [&](const uint4 raw, const bool first) {
+    // idle fast path: all 128 caps of the pass below the lowest threshold (union bin 0: nothing
+    // feasible for any policy) and the step before them in bin 0 too (or a block start), so no
+    // policy switches — 128 steps for bin 0 from one lane (night: most of C5's mixed steps)
+    const bool low = (int32_t)raw.x < t0 && (int32_t)raw.y < t0 && (int32_t)raw.z < t0 && (int32_t)raw.w < t0;
+    if (__all_sync(FULL, low) && (first || carry == 0u)) {
+      if (lane == 0) asm volatile("red.shared.add.u32 [%0], 128;" ::"r"(hA) : "memory");
+      carry = 0u;
+      if (first) bfirst = 0u;
+      return;
+    }
+    uint32_t b[4];
+    lut4_f32(L, raw, b, flags);
+    const uint32_t left = __shfl_sync(FULL, b[3], (lane + 31) & 31);
+    const uint32_t pb = lane == 0 ? (first ? b[0] : carry) : left;
+    carry = __shfl_sync(FULL, b[3], 31);
+    if (first) bfirst = b[0];
+    uint2 sg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sg[k] = s_sig2[b[k]];
+    const uint2 sp = pb == b[0] ? sg[0] : s_sig2[pb];
+    pk_count(hA, hW, dummy, b[0], sg[0], sp);
+    pk_count(hA, hW, dummy, b[1], sg[1], sg[0]);
+    pk_count(hA, hW, dummy, b[2], sg[2], sg[1]);
+    pk_count(hA, hW, dummy, b[3], sg[3], sg[2]);
+  };
+  int blk = wig;
+  if (blk < nblk) {
+    int v0 = blk * kPkBlkVec + lane;
+    uint4 r0 = ldv(v0), r1 = ldv(v0 + 32);
+    for (;;) {
+      const int vn = v0 + nwg * kPkBlkVec;  // this warp's next block
+      pass(r0, true);
+      r0 = ldv(vn);
+      pass(r1, false);
+      r1 = ldv(vn + 32);
+      if (lane == 0) edges[blk] = bfirst | (carry << 16);
+      if (blk + nwg >= nblk) break;
+      blk += nwg;
+      v0 = vn;
+    }
+    // the last block's fill steps, all in the bin of its last cap (= carry)
+    const int nfill = nblk * kPkBlkVec - nvf;
+    if (blk == nblk - 1 && lane == 0 && nfill > 0) atomicSub(&h[carry], 4u * (uint32_t)nfill);
+  }
+  // tail (< 4 caps at the very end of the trace)
+  for (int i = 4 * nvf + gtid; i < n; i += gsize) {
+    const uint32_t b = L.bin(__ldg(row + i), flags);
+    uint32_t dummyf = 0;
+    const uint32_t pb = i > 0 ? L.bin(__ldg(row + i - 1), dummyf) : b;  // step 0 is never penalised
+    pk_count(hA, hW, dummy, b, s_sig2[b], s_sig2[pb]);
+  }
+  return (flags & 1u) != 0u;
+}
+
+// PK epilogue: every aggregate of the trace from the touched bins only (a few hundred of C5's
+// 2,038), each reading its three selection segments from the staged signature — no prefix scan,
+// no pass over every segment. Per policy p and bin u with c steps of which s switched into u:
+// thr += (c - s) x thr_k + s x thr_k (1 - pf), energy += c x energy_k, k = seg_p(u), every value
+// split {hi, lo} with split_q exactly as prep_kernel does (sim.py:111, 119-122): the count x hi
+// products and their sums are exact. The block-boundary steps pk_main counted unswitched enter
+// as (c = 0, s = 1) corrections. Each warp compacts the nonzero bins of its 128-bin chunks into a
+// LIFO queue in its scratch and processes them 32 at a time with every lane busy; the bins are
+// re-zeroed on the way. Warp 0 writes the records and resets the counters: the only barrier is
+// the one before warp 0 combines the warps' partial sums (the next trace's first barrier orders
+// the scratch and counter reuse).
+//   sraw[k] = {thr (0 when idle), energy} per selection segment; sq[4p..4p+3] = {Q_thr, 1/Q_thr,
+//   Q_energy, 1/Q_energy} of policy p (shared)
+constexpr int kPkScrWarp = 40;  // doubles of scratch per warp: a 160-entry u16 queue / 24 partials
+
+template <bool STAGED, typename GH>
+__device__ __forceinline__ void pk_finish(const EvalParams& P, int64_t t, uint32_t* h, uint32_t* hw,
+                                          const uint32_t* edges, const uint2* s_sig2, uint32_t* vcnt, int vflag,
+                                          GH* ghist, const double2* sraw, const double* sq, double* scratch, int gtid,
+                                          int gsize, int gid_local) {
+  const int U = P.tb.U;
+  const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
+  const unsigned FULL = 0xffffffffu;
+  double a[3][4];
+  uint32_t idl[3] = {0u, 0u, 0u}, swc[3] = {0u, 0u, 0u};
+#pragma unroll
+  for (int p = 0; p < 3; ++p) a[p][0] = a[p][1] = a[p][2] = a[p][3] = 0.0;
+  auto acc = [&](int u, uint32_t c, const uint32_t (&ss)[3]) {
+    const uint2 sg = s_sig2[u];
+    const uint32_t kk[3] = {sg.x >> 16, sg.y, sg.x & 0xFFFFu};
+    const double dc = (double)c;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const double2 r = STAGED ? sraw[kk[p]] : __ldg(sraw + kk[p]);
+      const double q0 = sq[4 * p], q1 = sq[4 * p + 1];
+      if (c) {
+        const double2 ve = split_q(r.y, sq[4 * p + 2], sq[4 * p + 3]);
+        a[p][2] = __fma_rn(dc, ve.x, a[p][2]);
+        a[p][3] = __fma_rn(dc, ve.y, a[p][3]);
+      }
+      swc[p] += ss[p];
+      if (u < P.fidle[p]) {
+        idl[p] += c;  // idle selection: zero throughput, switched or not
+      } else {
+        const double2 vt = split_q(r.x, q0, q1);
+        const double dn = (double)((int32_t)c - (int32_t)ss[p]);
+        a[p][0] = __fma_rn(dn, vt.x, a[p][0]);
+        a[p][1] = __fma_rn(dn, vt.y, a[p][1]);
+        if (ss[p]) {
+          const double ds = (double)ss[p];
+          const double2 vp = split_q(__dmul_rn(r.x, P.omp), q0, q1);
+          a[p][0] = __fma_rn(ds, vp.x, a[p][0]);
+          a[p][1] = __fma_rn(ds, vp.y, a[p][1]);
+        }
+      }
+    }
+  };
+  // (1) switches across block boundaries (a block's first step was counted unswitched)
+  const int nblk = ((int)(P.S >> 2) + kPkBlkVec - 1) / kPkBlkVec;
+  for (int i = gtid + 1; i < nblk; i += gsize) {
+    const uint32_t b = edges[i] & 0xFFFFu, pb = edges[i - 1] >> 16;
+    if (b != pb) {
+      const uint2 sc = s_sig2[b], sp = s_sig2[pb];
+      const uint32_t x = sc.x ^ sp.x;
+      const uint32_t ss[3] = {(x >> 16) ? 1u : 0u, sc.y != sp.y ? 1u : 0u, (x & 0xFFFFu) ? 1u : 0u};
+      if (ss[0] | ss[1] | ss[2]) acc((int)b, 0u, ss);
+    }
+  }
+  // (2) the touched bins, 4 per lane per chunk, compacted through the warp's LIFO queue
+  uint16_t* q = reinterpret_cast<uint16_t*>(scratch + wig * kPkScrWarp);
+  auto bin = [&](int u) {
+    const uint32_t wa = h[u], wb = hw[u];
+    h[u] = 0u;
+    hw[u] = 0u;
+    const uint32_t c = wa & 0xFFFFu;
+    if (ghist) atomicAdd(&ghist[u], (GH)c);
+    const uint32_t ss[3] = {wb >> 16, wa >> 16, wb & 0xFFFFu};
+    acc(u, c, ss);
+  };
+  const uint32_t lt = (1u << lane) - 1u;
+  int n = 0;
+  for (int base = wig * 128; base < U; base += 128 * nw) {
+    const int u = base + 4 * lane;
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (u < U) w = *reinterpret_cast<const uint4*>(h + u);  // h[U..U4) stay zero
+    const uint32_t m = (w.x ? 1u : 0u) | (w.y ? 2u : 0u) | (w.z ? 4u : 0u) | (w.w ? 8u : 0u);
+    const uint32_t c = __popc(m);
+    const uint32_t b0 = __ballot_sync(FULL, c & 1u), b1 = __ballot_sync(FULL, c & 2u),
+                   b2 = __ballot_sync(FULL, c & 4u);
+    int pos = n + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+    if (m & 1u) q[pos++] = (uint16_t)u;
+    if (m & 2u) q[pos++] = (uint16_t)(u + 1);
+    if (m & 4u) q[pos++] = (uint16_t)(u + 2);
+    if (m & 8u) q[pos] = (uint16_t)(u + 3);
+    n += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+    __syncwarp();
+    while (n >= 32) {
+      n -= 32;
+      bin(q[n + lane]);
+    }
+    __syncwarp();
+  }
+  if (lane < n) bin(q[lane]);
+  __syncwarp();
+  // (3) reduce and write: warp 0 combines the group's partial sums (one barrier)
+  double mine[3];
+  uint32_t ired[6];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    mine[p] = xreduce4(a[p], lane);
+    ired[p] = __reduce_add_sync(FULL, idl[p]);
+    ired[3 + p] = __reduce_add_sync(FULL, swc[p]);
+  }
+  if (nw > 1) {
+    double* d = scratch + wig * kPkScrWarp;
+    if (wig > 0) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (lane == kLaneOf4[c]) d[4 * p + c] = mine[p];
+      if (lane == 0)
+        for (int j = 0; j < 6; ++j) d[12 + j] = __longlong_as_double((long long)ired[j]);
+    }
+    group_sync(gid_local, gsize);
+    if (wig > 0) return;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (lane == kLaneOf4[c])
+          for (int w = 1; w < nw; ++w) mine[p] = __dadd_rn(mine[p], scratch[w * kPkScrWarp + 4 * p + c]);
+    for (int w = 1; w < nw; ++w)
+      for (int j = 0; j < 6; ++j) ired[j] += (uint32_t)__double_as_longlong(scratch[w * kPkScrWarp + 12 + j]);
+  }
+  double part[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double x0 = __shfl_sync(FULL, mine[0], kLaneOf4[c]);
+    const double x1 = __shfl_sync(FULL, mine[1], kLaneOf4[c]);
+    const double x2 = __shfl_sync(FULL, mine[2], kLaneOf4[c]);
+    part[c] = lane == 0 ? x0 : (lane == 1 ? x1 : x2);
+  }
+  if (lane < 3) {
+    dd tsum{part[0], 0.0}, esum{part[2], 0.0};
+    dd_add2(tsum, part[1], 0.0);
+    dd_add2(esum, part[3], 0.0);
+    cs_agg r;
+    r.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
+    r.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
+    r.idle_steps = lane == 0 ? ired[0] : (lane == 1 ? ired[1] : ired[2]);
+    r.switches = lane == 0 ? ired[3] : (lane == 1 ? ired[4] : ired[5]);
+    r.violations = vcnt[lane];
+    r.num_steps = P.S;
+    if (P.agg) P.agg[t * 3 + lane] = r;
+  }
+  __syncwarp();
+  if (lane < 3) vcnt[lane] = 0u;  // recounts of the next trace come after its first barrier
+  if (lane == 0) vcnt[3 + vflag] = 0u;
 }
 
 // fp64 LUT search (cs_internal.h encoding) with thresholds and LUT in shared memory; leaves' bit 14
@@ -1127,14 +1266,11 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   double2* s_segval = reinterpret_cast<double2*>(s_segidle + ((M * 3 + 3) & ~3));
   double2* s_binval = reinterpret_cast<double2*>(smem + P.off_seg);
   double2* s_pkraw = reinterpret_cast<double2*>(smem + P.off_seg);  // PK: {thr, energy} per segment
-  double* s_pkq = reinterpret_cast<double*>(s_pkraw + P.NSEG);         //     + the 3 policies' quanta
-  const double2* pk_raw = seg_staged ? s_pkraw : P.seg_raw;
-  const double* pk_q = seg_staged ? s_pkq : P.seg_q;
+  double* s_pkq = reinterpret_cast<double*>(smem + P.off_pkq);         //     the 3 policies' quanta
   if (PK) {
-    if (seg_staged) {
+    if (seg_staged)
       for (int i = threadIdx.x; i < P.NSEG; i += blockDim.x) s_pkraw[i] = __ldg(P.seg_raw + i);
-      if (threadIdx.x < 12) s_pkq[threadIdx.x] = __ldg(P.seg_q + threadIdx.x);
-    }
+    if (threadIdx.x < 12) s_pkq[threadIdx.x] = __ldg(P.seg_q + threadIdx.x);
   } else if (!PEN && P.bin_epi) {
     for (int i = threadIdx.x; i < 6 * P.U4; i += blockDim.x) s_binval[i] = __ldg(P.bin_val + i);
   } else if (seg_staged) {
@@ -1161,6 +1297,8 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
   if (gtid < M * 3) vcnt[gtid] = 0u;
   if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag (the plan keeps 3M < group size)
+  if (PK && gtid == 0) vcnt[M * 3 + 1] = 0u;  // PK: flags alternate between traces
+  uint32_t* edges = reinterpret_cast<uint32_t*>(gbase + P.off_g_edge);
   __syncthreads();
 
   Lut64 L64;
@@ -1183,13 +1321,46 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
 
   const int64_t n_items = P.T * (int64_t)P.nseg;
   const int64_t n_groups = (int64_t)gridDim.x * P.gpc;
-  for (int64_t item = (int64_t)blockIdx.x * P.gpc + gid_local; item < n_items; item += n_groups) {
+  int iter = 0;
+  for (int64_t item = (int64_t)blockIdx.x * P.gpc + gid_local; item < n_items; item += n_groups, ++iter) {
+    if constexpr (PK) {  // whole traces (nseg == 1), two barriers per trace (pk_finish)
+      const int64_t t = item;
+      const int vflag = iter & 1;
+      const bool bad = pk_main(P, L, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), t, gtid, gsize);
+      if (VIO && bad) atomicOr(&vcnt[3 + vflag], 1u);
+      group_sync(gid_local, gsize);
+      if (VIO && vcnt[3 + vflag]) {  // never taken when the tables are right: exact recount
+        const CapT* row = reinterpret_cast<const CapT*>(P.caps) + t * P.ld;
+        recount_violations<CapT>(P, s_lut, row, 0, P.S, vcnt, gtid, gsize);
+        group_sync(gid_local, gsize);
+      }
+      if (want_hist) {
+        uint32_t before = 0;
+        if (gtid == 0) before = atomicAdd(s_gsteps, (uint32_t)P.S);
+        before = __shfl_sync(0xffffffffu, before, 0);
+        if (before > (1u << 31) && gtid < 32) {  // rare: drain the 32-bit counters (this warp)
+          if (gtid == 0) atomicExch(s_gsteps, 0u);
+          for (int u = gtid; u < U; u += 32) {
+            const uint32_t c = atomicExch(&s_ghist[u], 0u);
+            if (c) atomicAdd(P.hist + u, (unsigned long long)c);
+          }
+        }
+      }
+      uint32_t* gh = want_hist ? s_ghist : (uint32_t*)nullptr;
+      if (seg_staged)
+        pk_finish<true>(P, t, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), vcnt, vflag, gh, s_pkraw, s_pkq,
+                        scratch, gtid, gsize, gid_local);
+      else
+        pk_finish<false>(P, t, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), vcnt, vflag, gh, P.seg_raw,
+                         s_pkq, scratch, gtid, gsize, gid_local);
+      continue;
+    }
     const int64_t t = item / P.nseg;
     const int64_t s0 = (item - t * P.nseg) * P.seg_len;
     const int64_t s1e = min(P.S, s0 + P.seg_len);
     bool bad;
     if constexpr (F32)
-      bad = run_segment_f32<PEN, STEP, VIO, UNI, PK>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+      bad = run_segment_f32<PEN, STEP, VIO, UNI>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     else
       bad = run_segment_f64<PEN, STEP, VIO>(P, L64, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     if (VIO && bad) atomicOr(&vcnt[M * 3], 1u);
@@ -1215,10 +1386,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
         }
       }
       uint32_t* gh = want_hist ? s_ghist : (uint32_t*)nullptr;
-      if (PK) {
-        finish_trace_pk(P, t, h, sw, reinterpret_cast<const uint2*>(s_sig), vcnt, gh, pk_raw, pk_q, scratch, gtid,
-                        gsize, gid_local);
-      } else if (!PEN && P.bin_epi)
+      if (!PEN && P.bin_epi)
         finish_trace_bins(P, t, h, vcnt, gh, s_binval, scratch, gtid, gsize, gid_local);
       else if (seg_staged)  // two instantiations so each reads its tables with a known address space
         finish_trace<PEN, false>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
@@ -1372,8 +1540,11 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   // PK: 16-bit packed step / switched-step counters need < 2^16 steps per trace (whole traces per
   // group; re-planned without it when the plan splits traces); CS_PLAN_NO_PK: tuning only
   static const bool no_pk_env = std::getenv("CS_PLAN_NO_PK") != nullptr;
+  // (the last block's fill steps count too: < 4 kPkBlkVec of them)
   const bool pk = allow_pk && !no_pk_env && f32 && pen && M == 1 && a->step_bins == nullptr &&
-                  a->n_steps <= 0xFFFF && !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
+                  a->n_steps <= 0xFFFF - 4 * kPkBlkVec && !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
+  const int pk_nblk = pk ? (int)((a->n_steps / 4 + kPkBlkVec - 1) / kPkBlkVec) : 0;
+  const size_t pkq_bytes = pk ? 128 : 0;  // the 3 policies' quanta (12 doubles)
   void* fn = pick_kernel(f32, pen, a->step_bins != nullptr, vio, false, pk);
   int smem_optin = 232448;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1395,7 +1566,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   const bool bin_epi = !pen && M == 1 && (double)a->n_traces * (double)a->n_steps >= (double)(1 << 22) &&
                        !(a->flags & CS_FLAG_SEGMENT_EPILOGUE);
   const size_t bin_bytes = (size_t)6 * U4 * 16;
-  const size_t seg_smem = pk        ? a16((size_t)nsegs * 16 + 12 * 8)  // PK: {thr, energy} per segment + quanta
+  const size_t seg_smem = pk        ? a16((size_t)nsegs * 16)  // PK: {thr, energy} per segment
                           : bin_epi ? bin_bytes
                                     : a16(seg_hdr_b + seg_idle_b + (size_t)(pen ? 6 : 4) * nsegs * 8);
   auto group_bytes = [&](int wpg, size_t* off_sw, size_t* off_v, size_t* off_scr) {
@@ -1404,9 +1575,10 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     // PK: the second packed word per bin; else + 32 dummy slots (branch-free switch counting)
     gb += pk ? a16((size_t)(U4 + 32) * 4) : pen ? a16((size_t)(nsegs + 32) * 4) : 0;
     *off_v = gb;
-    gb += a16((size_t)(M * 3 + 1) * 4);
+    gb += a16((size_t)(M * 3 + 2) * 4);
+    if (pk) gb += a16((size_t)pk_nblk * 4);  // block edges (pk_main)
     *off_scr = gb;
-    gb += (size_t)wpg * 24 * 8;
+    gb += (size_t)wpg * (pk ? kPkScrWarp : 24) * 8;
     return a16(gb);
   };
   // candidates: most resident warps per SM first, then the smallest worker group; the segment
@@ -1424,7 +1596,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   static const int force_wpg = std::getenv("CS_PLAN_WPG") ? std::atoi(std::getenv("CS_PLAN_WPG")) : 0;  // tuning only
   auto search = [&](size_t lut_b) {
     Cand b;
-    const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;
+    const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes + pkq_bytes;
     for (int staged = small ? 0 : 1; staged >= 0; --staged)
       for (int threads : {1024, 512, 256, 128}) {
         for (int wpg : {1, 2, 4, 8, 16, 32}) {
@@ -1445,7 +1617,11 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
           const int per_sm = blocks_per_sm(fn, dev, threads, smem);
           if (per_sm < 1) continue;
           const int warps = tiny ? wpc : per_sm * wpc;  // tiny: the biggest CTA, it runs alone
-          if (warps > b.warps || (warps == b.warps && wpg < b.wpg && staged == (int)b.staged)) {
+          // PK: the smaller worker group wins even unstaged — its per-trace barriers and epilogue
+          // cost more than reading the compact segment pairs through L1 (C5: 4-warp groups with
+          // the tables in global memory 2.64 ms, 8-warp groups staged 3.23 ms)
+          if (warps > b.warps ||
+              (warps == b.warps && wpg < b.wpg && (pk || staged == (int)b.staged))) {
             b.warps = warps, b.threads = threads, b.wpg = wpg, b.per_sm = per_sm, b.smem = smem;
             b.staged = staged != 0;
           }
@@ -1462,7 +1638,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     if (cb.warps >= c.warps && cb.warps > 0 && cb.wpg <= c.wpg && (cb.staged || !c.staged)) c = cb, big = true;
   }
   const size_t lut_b = big ? a16((size_t)view.n_lut_big * 4) : lut_bytes;  // the LUT staged
-  const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes;
+  const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes + pkq_bytes;
   int best_warps = c.warps, b_threads = c.threads, b_wpg = c.wpg, b_per_sm = c.per_sm;
   size_t b_smem = c.smem;
   bool b_staged = c.staged;
@@ -1529,6 +1705,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_vio = (int32_t)lut_b;
   P.off_sig = (int32_t)(lut_b + vio_bytes);
   P.off_ghist = (int32_t)(lut_b + vio_bytes + sig_bytes);
+  P.off_pkq = (int32_t)(lut_b + vio_bytes + sig_bytes + gh_bytes);
   P.off_seg = (int32_t)fixed0;
   P.seg_smem_bytes = b_staged ? (int32_t)seg_smem : 0;
   P.bin_epi = (bin_epi && b_staged) ? 1 : 0;  // only with its tables in shared memory
@@ -1543,6 +1720,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_g_sw = (int32_t)o1;
   P.off_g_vio = (int32_t)o2;
   P.off_g_scr = (int32_t)o3;
+  P.off_g_edge = (int32_t)(o2 + a16((size_t)(M * 3 + 2) * 4));
   return std::string();
 }
 

@@ -166,7 +166,7 @@ def test_c5_plan_packed_penalty(cs, torch, kind, pen):
     import bench
 
     grids = bench.make_grids("fine")
-    T, S, step = 2048, 10080, 60  # 20.6M timesteps: whole traces per worker group
+    T, S, step = 2400, 10080, 60  # 24.2M timesteps: whole traces per worker group (>= 2 per group)
     caps = cs.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306)
     torch.cuda.synchronize()
     caps_np = caps[:, :S].cpu().numpy()
@@ -189,17 +189,19 @@ def test_c5_plan_packed_penalty(cs, torch, kind, pen):
     assert torch.allclose(res.energy_proxy_wh, old.energy_proxy_wh, rtol=1e-12, atol=0)
 
 
-def test_pk_short_traces_and_tails(cs, torch):
-    """PK with ragged lengths (tails of < 4 caps, warp chunks that end mid-pass), a trace of one
-    step, and the plan falling back when a trace would be split (few traces)."""
+@pytest.mark.parametrize("kind", ["iid", "mixed"])
+def test_pk_short_traces_and_tails(cs, torch, kind):
+    """PK with ragged lengths (tails of < 4 caps, last blocks partly filled with the last cap,
+    whole blocks only: 1280 steps), a trace of one step, and the plan falling back when a trace
+    would be split (few traces)."""
     import bench
     from oracle import oracle
 
     grids = bench.make_grids("fine")
     og = bench.oracle_grids(grids)
     tables = cs.Tables.stage(grids, "f32")
-    for T, S in ((4800, 1023), (4800, 5), (4800, 1), (3, 9000)):
-        caps = cs.generate_traces(T, S, step_seconds=60, kind="iid", seed=11)
+    for T, S in ((4800, 1023), (4800, 5), (4800, 1), (4800, 1280), (4800, 2305), (3, 9000)):
+        caps = cs.generate_traces(T, S, step_seconds=60, kind=kind, seed=11)
         torch.cuda.synchronize()
         res = tables.evaluate(caps, S, step_seconds=60, switch_penalty_s=10.0)
         torch.cuda.synchronize()
