@@ -878,9 +878,12 @@ __device__ __forceinline__ bool pk_main(const EvalParams& P, const Lut32& L, uin
   const uint32_t dummy = hW + 4u * (uint32_t)(P.U4 + lane);
   const int32_t t0 = P.t0_bits;
   uint32_t flags = 0;
-  auto ldv = [&](int v) -> uint4 {
-    const uint4 r = ldg_stream(vrow + min(v, nvf - 1));
-    return v < nvf ? r : make_uint4(r.w, r.w, r.w, r.w);
+  // loads clamp to the last full vector; the fill replaces them with its last cap only when the
+  // block is the trace's last (a select right after the load would wait for it: the compiler
+  // placed it there, stalling every prefetch)
+  auto ldv = [&](int v) -> uint4 { return ldg_stream(vrow + min(v, nvf - 1)); };
+  auto fill = [&](uint4& r, int v) {
+    if (v >= nvf) r = make_uint4(r.w, r.w, r.w, r.w);
   };
   uint32_t carry = 0u, bfirst = 0u;
   auto pass = [&](const uint4 raw, const bool first) {
@@ -915,6 +918,10 @@ __device__ __forceinline__ bool pk_main(const EvalParams& P, const Lut32& L, uin
     uint4 r0 = ldv(v0), r1 = ldv(v0 + 32);
     for (;;) {
       const int vn = v0 + nwg * kPkBlkVec;  // this warp's next block
+      if (blk == nblk - 1) {  // warp-uniform
+        fill(r0, v0);
+        fill(r1, v0 + 32);
+      }
       pass(r0, true);
       r0 = ldv(vn);
       pass(r1, false);
