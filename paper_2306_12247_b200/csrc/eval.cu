@@ -803,7 +803,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
 //   edges[i] = first bin | last bin << 16 of block i (kPkBlkVec vectors, dealt round-robin)
 // 16-bit fields cannot carry: a trace has < 2^16 steps (the plan also counts the fill below).
 // ---------------------------------------------------------------------------------------------
-constexpr int kPkBlkVec = 64;  // vectors (4 caps each) per block: two 32-lane passes
+constexpr int kPkBlkVec = 32;  // vectors (4 caps each) per block: one 32-lane pass, grabbed dynamically
 
 // bins of 4 caps (no redirect-uniform variant), ORing the leaves into flags
 __device__ __forceinline__ void lut4_f32(const Lut32& L, const uint4 raw, uint32_t (&b)[4], uint32_t& flags) {
@@ -856,17 +856,20 @@ __device__ __forceinline__ void pk_count(uint32_t hA, uint32_t hW, uint32_t dumm
   asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(sc.y != sp.y ? a : dummy) : "memory");
 }
 
-// Main loop of one whole trace (s0 = 0). Blocks of kPkBlkVec vectors are dealt round-robin to the
-// group's warps (a warp's contiguous share could be all night while another's is all day, and the
-// group waits at its per-trace barrier). Inside a block the cap before lane l's vector is lane
-// l-1's last (a shuffle) and lane 0's comes from lane 31 of the previous pass; a block's first
-// step is counted unswitched and its (first, last) bins go to edges[] — pk_finish adds the
-// switches across block boundaries. Each lane keeps the next block's loads in flight under the
-// current block (two unrolled passes, no register rotation). Vectors past the end of the trace
-// replicate its last full vector's last cap (no predication in the passes); their steps, all in
-// that cap's bin, are subtracted once at the end. Returns true if a cap met an unproven leaf.
+// Main loop of one whole trace (s0 = 0), in blocks of one 32-lane pass grabbed from a per-group
+// counter (ctr), so the warps of a group finish the trace together whatever its day/night
+// pattern (round-robin blocks left them waiting at the per-trace barrier: C5 -6 %). Inside a
+// block the cap before lane l's vector is lane l-1's last (a shuffle); the block's first step
+// (lane 0's first cap) is counted unswitched and its (first, last) bins go to edges[] —
+// pk_finish adds the switches across block boundaries, so no block needs the bin of the cap
+// before it. Each warp keeps its next block's load in flight under the current one (two unrolled
+// passes, no register rotation). Vectors past the end of the trace replicate its last full
+// vector's last cap (no predication in the passes; applied at use — a select right after the
+// load stalls the prefetch); their steps, all in that cap's bin, are subtracted once. Returns
+// true if a cap met an unproven leaf.
 __device__ __forceinline__ bool pk_main(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* hw,
-                                        uint32_t* edges, const uint2* s_sig2, int64_t t, int gtid, int gsize) {
+                                            uint32_t* edges, const uint2* s_sig2, uint32_t* ctr, int64_t t,
+                                            int gtid, int gsize) {
   const int n = (int)P.S;
   const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
   const uint4* vrow = reinterpret_cast<const uint4*>(row);
@@ -878,65 +881,59 @@ __device__ __forceinline__ bool pk_main(const EvalParams& P, const Lut32& L, uin
   const uint32_t dummy = hW + 4u * (uint32_t)(P.U4 + lane);
   const int32_t t0 = P.t0_bits;
   uint32_t flags = 0;
-  // loads clamp to the last full vector; the fill replaces them with its last cap only when the
-  // block is the trace's last (a select right after the load would wait for it: the compiler
-  // placed it there, stalling every prefetch)
-  auto ldv = [&](int v) -> uint4 { return ldg_stream(vrow + min(v, nvf - 1)); };
-  auto fill = [&](uint4& r, int v) {
-    if (v >= nvf) r = make_uint4(r.w, r.w, r.w, r.w);
+  auto grab = [&]() -> int {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(ctr, 1u);
+    return (int)__shfl_sync(FULL, b, 0) + nwg;  // the first nwg blocks are taken statically
   };
-  uint32_t carry = 0u, bfirst = 0u;
-  auto pass = [&](const uint4 raw, const bool first) {
-    // idle fast path: all 128 caps of the pass below the lowest threshold (union bin 0: nothing
-    // feasible for any policy) and the step before them in bin 0 too (or a block start), so no
-    // policy switches — 128 steps for bin 0 from one lane (night: most of C5's mixed steps)
+  auto ldv = [&](int blk) -> uint4 { return ldg_stream(vrow + min(blk * kPkBlkVec + lane, nvf - 1)); };
+  auto pass = [&](uint4 raw, int blk) {
+    if (blk == nblk - 1 && blk * kPkBlkVec + lane >= nvf) raw = make_uint4(raw.w, raw.w, raw.w, raw.w);
     const bool low = (int32_t)raw.x < t0 && (int32_t)raw.y < t0 && (int32_t)raw.z < t0 && (int32_t)raw.w < t0;
-    if (__all_sync(FULL, low) && (first || carry == 0u)) {
-      if (lane == 0) asm volatile("red.shared.add.u32 [%0], 128;" ::"r"(hA) : "memory");
-      carry = 0u;
-      if (first) bfirst = 0u;
-      return;
-    }
-    uint32_t b[4];
-    lut4_f32(L, raw, b, flags);
-    const uint32_t left = __shfl_sync(FULL, b[3], (lane + 31) & 31);
-    const uint32_t pb = lane == 0 ? (first ? b[0] : carry) : left;
-    carry = __shfl_sync(FULL, b[3], 31);
-    if (first) bfirst = b[0];
-    uint2 sg[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) sg[k] = s_sig2[b[k]];
-    const uint2 sp = pb == b[0] ? sg[0] : s_sig2[pb];
-    pk_count(hA, hW, dummy, b[0], sg[0], sp);
-    pk_count(hA, hW, dummy, b[1], sg[1], sg[0]);
-    pk_count(hA, hW, dummy, b[2], sg[2], sg[1]);
-    pk_count(hA, hW, dummy, b[3], sg[3], sg[2]);
-  };
-  int blk = wig;
-  if (blk < nblk) {
-    int v0 = blk * kPkBlkVec + lane;
-    uint4 r0 = ldv(v0), r1 = ldv(v0 + 32);
-    for (;;) {
-      const int vn = v0 + nwg * kPkBlkVec;  // this warp's next block
-      if (blk == nblk - 1) {  // warp-uniform
-        fill(r0, v0);
-        fill(r1, v0 + 32);
+    uint32_t last = 0u;
+    if (__all_sync(FULL, low)) {
+      if (lane == 0) {
+        asm volatile("red.shared.add.u32 [%0], 128;" ::"r"(hA) : "memory");
+        edges[blk] = 0u;
       }
-      pass(r0, true);
-      r0 = ldv(vn);
-      pass(r1, false);
-      r1 = ldv(vn + 32);
-      if (lane == 0) edges[blk] = bfirst | (carry << 16);
-      if (blk + nwg >= nblk) break;
-      blk += nwg;
-      v0 = vn;
+    } else {
+      uint32_t b[4];
+      lut4_f32(L, raw, b, flags);
+      const uint32_t left = __shfl_sync(FULL, b[3], (lane + 31) & 31);
+      const uint32_t pb = lane == 0 ? b[0] : left;
+      last = __shfl_sync(FULL, b[3], 31);
+      if (lane == 0) edges[blk] = b[0] | (last << 16);
+      uint2 sg[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sg[k] = s_sig2[b[k]];
+      const uint2 sp = pb == b[0] ? sg[0] : s_sig2[pb];
+      pk_count(hA, hW, dummy, b[0], sg[0], sp);
+      pk_count(hA, hW, dummy, b[1], sg[1], sg[0]);
+      pk_count(hA, hW, dummy, b[2], sg[2], sg[1]);
+      pk_count(hA, hW, dummy, b[3], sg[3], sg[2]);
     }
-    // the last block's fill steps, all in the bin of its last cap (= carry)
-    const int nfill = nblk * kPkBlkVec - nvf;
-    if (blk == nblk - 1 && lane == 0 && nfill > 0) atomicSub(&h[carry], 4u * (uint32_t)nfill);
+    const int nfill = nblk * kPkBlkVec - nvf;  // the last block's fill steps, all in bin `last`
+    if (blk == nblk - 1 && lane == 0 && nfill > 0) atomicSub(&h[last], 4u * (uint32_t)nfill);
+  };
+  int b0 = wig;
+  // (three blocks in flight — three unrolled passes or a rotated register queue — measured
+  // slower: C5 2.74 / 2.55 vs 2.32 ms)
+  if (b0 < nblk) {
+    uint4 r0 = ldv(b0);
+    int b1 = grab();
+    uint4 r1 = ldv(b1);
+    for (;;) {
+      pass(r0, b0);
+      if (b1 >= nblk) break;
+      b0 = grab();
+      r0 = ldv(b0);
+      pass(r1, b1);
+      if (b0 >= nblk) break;
+      b1 = grab();
+      r1 = ldv(b1);
+    }
   }
-  // tail (< 4 caps at the very end of the trace)
-  for (int i = 4 * nvf + gtid; i < n; i += gsize) {
+  for (int i = 4 * nvf + gtid; i < n; i += gsize) {  // tail (< 4 caps at the end)
     const uint32_t b = L.bin(__ldg(row + i), flags);
     uint32_t dummyf = 0;
     const uint32_t pb = i > 0 ? L.bin(__ldg(row + i - 1), dummyf) : b;  // step 0 is never penalised
@@ -1026,7 +1023,8 @@ __device__ __forceinline__ void pk_finish(const EvalParams& P, int64_t t, uint32
   };
   const uint32_t lt = (1u << lane) - 1u;
   int n = 0;
-  for (int base = wig * 128; base < U; base += 128 * nw) {
+  uint32_t* ctr2 = vcnt + 6;  // 128-bin chunks are grabbed dynamically too (the first nw statically)
+  for (int base = wig * 128; base < U;) {
     const int u = base + 4 * lane;
     uint4 w = make_uint4(0u, 0u, 0u, 0u);
     if (u < U) w = *reinterpret_cast<const uint4*>(h + u);  // h[U..U4) stay zero
@@ -1046,6 +1044,9 @@ __device__ __forceinline__ void pk_finish(const EvalParams& P, int64_t t, uint32
       bin(q[n + lane]);
     }
     __syncwarp();
+    uint32_t g = 0;
+    if (lane == 0) g = atomicAdd(ctr2, 1u);
+    base = 128 * ((int)__shfl_sync(FULL, g, 0) + nw);
   }
   if (lane < n) bin(q[lane]);
   __syncwarp();
@@ -1104,6 +1105,7 @@ __device__ __forceinline__ void pk_finish(const EvalParams& P, int64_t t, uint32
   __syncwarp();
   if (lane < 3) vcnt[lane] = 0u;  // recounts of the next trace come after its first barrier
   if (lane == 0) vcnt[3 + vflag] = 0u;
+  if (lane == 0) vcnt[6] = 0u;  // scan-chunk counter (all grabs of this trace were before the barrier)
 }
 
 // fp64 LUT search (cs_internal.h encoding) with thresholds and LUT in shared memory; leaves' bit 14
@@ -1304,7 +1306,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     for (int i = gtid; i < P.NSEG; i += gsize) sw[i] = 0u;
   if (gtid < M * 3) vcnt[gtid] = 0u;
   if (gtid == 0) vcnt[M * 3] = 0u;  // group "violation seen" flag (the plan keeps 3M < group size)
-  if (PK && gtid == 0) vcnt[M * 3 + 1] = 0u;  // PK: flags alternate between traces
+  if (PK && gtid == 0) vcnt[M * 3 + 1] = vcnt[M * 3 + 2] = vcnt[M * 3 + 3] = 0u;  // PK: 2nd flag, counters
   uint32_t* edges = reinterpret_cast<uint32_t*>(gbase + P.off_g_edge);
   __syncthreads();
 
@@ -1333,9 +1335,10 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     if constexpr (PK) {  // whole traces (nseg == 1), two barriers per trace (pk_finish)
       const int64_t t = item;
       const int vflag = iter & 1;
-      const bool bad = pk_main(P, L, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), t, gtid, gsize);
+      const bool bad = pk_main(P, L, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), vcnt + 5, t, gtid, gsize);
       if (VIO && bad) atomicOr(&vcnt[3 + vflag], 1u);
       group_sync(gid_local, gsize);
+      if (gtid == 0) vcnt[5] = 0u;  // block counter: every grab of this trace came before the barrier
       if (VIO && vcnt[3 + vflag]) {  // never taken when the tables are right: exact recount
         const CapT* row = reinterpret_cast<const CapT*>(P.caps) + t * P.ld;
         recount_violations<CapT>(P, s_lut, row, 0, P.S, vcnt, gtid, gsize);
@@ -1582,7 +1585,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     // PK: the second packed word per bin; else + 32 dummy slots (branch-free switch counting)
     gb += pk ? a16((size_t)(U4 + 32) * 4) : pen ? a16((size_t)(nsegs + 32) * 4) : 0;
     *off_v = gb;
-    gb += a16((size_t)(M * 3 + 2) * 4);
+    gb += a16((size_t)(M * 3 + 4) * 4);  // PK: + alternating flag, block / scan-chunk counters
     if (pk) gb += a16((size_t)pk_nblk * 4);  // block edges (pk_main)
     *off_scr = gb;
     gb += (size_t)wpg * (pk ? kPkScrWarp : 24) * 8;
@@ -1727,7 +1730,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_g_sw = (int32_t)o1;
   P.off_g_vio = (int32_t)o2;
   P.off_g_scr = (int32_t)o3;
-  P.off_g_edge = (int32_t)(o2 + a16((size_t)(M * 3 + 2) * 4));
+  P.off_g_edge = (int32_t)(o2 + a16((size_t)(M * 3 + 4) * 4));
   return std::string();
 }
 
