@@ -576,7 +576,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
         count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], 0, 0, 0, sw_s, sw_dummy);
   };
   // union bins of one 16-B vector (4 caps) into b[] (LUT search only)
-  auto lut4 = [&](const uint4 raw, uint32_t (&b)[4]) {
+  auto lut4 = [&](const uint4 raw, uint32_t (&b)[4], const unsigned vmask) {
     const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t e[4];
 #pragma unroll
@@ -591,7 +591,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     // UNI (redirect-heavy tables: many multi-threshold buckets): a warp with any redirecting lane
     // runs only the redirect path (correct for plain leaves too) instead of both sides of a
     // divergent branch — C3 +3-6 %; with sparse redirects the per-lane branch is cheaper (C4)
-    const bool plain = UNI ? !__any_sync(__activemask(), (int32_t)any < 0) : (int32_t)any >= 0;
+    const bool plain = UNI ? !__any_sync(vmask, (int32_t)any < 0) : (int32_t)any >= 0;
     if (plain) {  // no redirect (marker 0xFFF.....; leaves have bit 31 clear while U < 2^15)
       if (VIO) flags |= any;
 #pragma unroll
@@ -601,6 +601,17 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       // at shift s1 - 4 (staging.cpp: LutBuilder::make), so shift and leaf mask are constants —
       // then the general loop only for chains (rare)
       uint32_t msk[4];
+      if (UNI) {  // branch-free: every element loads (non-redirects read entry 0, a broadcast;
+                  // the predicated loads compiled to four divergent branches: C3 +2.4 %, iid +5.7 %)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool r = e[k] >= kRedirect32;
+          const uint32_t i = r ? L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> L.s2) & 15u) : 0u;
+          const uint32_t e2 = L.lut[i];
+          msk[k] = r ? L.mask2 : L.mask1;
+          e[k] = r ? e2 : e[k];
+        }
+      } else
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         msk[k] = L.mask1;
@@ -624,8 +635,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     }
   };
   // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
-  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4]) {
-    lut4(raw, b);
+  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4], const unsigned vmask = 0xffffffffu) {
+    lut4(raw, b, vmask);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
 #ifdef CS_DIAG_NO_ATOMS  // diagnostic build only: no histogram update (wrong aggregates)
@@ -677,7 +688,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     auto pass = [&](const uint4 raw, int v) {
       uint32_t b[4] = {0u, 0u, 0u, 0u};
       const bool act = v < ve;
-      if (act) bins4(raw, v, b);
+      if (act) bins4(raw, v, b, __activemask());
       const uint32_t left = __shfl_sync(0xffffffffu, b[3], (lane + 31) & 31);
       uint32_t pb = lane == 0 ? carry : left;
       carry = __shfl_sync(0xffffffffu, b[3], 31);
@@ -708,9 +719,10 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       pass(r, v);
     }
   } else {
-    auto vec4 = [&](const uint4 raw, int v) {
+    // (full warps in the main loops: the redirect vote needs no __activemask)
+    auto vec4 = [&](const uint4 raw, int v, const unsigned vmask = 0xffffffffu) {
       uint32_t b[4];
-      bins4(raw, v, b);
+      bins4(raw, v, b, vmask);
     };
     int v = gtid;
 #ifdef CS_TC
@@ -779,7 +791,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       vec4(r2, v + 2 * gsize);
       vec4(r3, v + 3 * gsize);
     }
-    for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
+    for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v, __activemask());
   }
   // tail (< 4 caps at the very end of a trace)
   for (int i = 4 * nvf + gtid; i < n; i += gsize) {
