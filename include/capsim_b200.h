@@ -87,6 +87,9 @@ typedef struct {
   int32_t lut_big_entries; /* fp32: finer LUT that cs_eval stages when shared memory allows (0: none) */
   int32_t lut_big_shift;
   int32_t lut_big_unsafe_leaves;
+  int32_t lut_huge_entries; /* fp32: finer still, for thousands of union thresholds (0: none) */
+  int32_t lut_huge_shift;
+  int32_t lut_huge_unsafe_leaves;
 } cs_tables_info;
 
 typedef struct cs_tables cs_tables;

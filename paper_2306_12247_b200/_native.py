@@ -102,6 +102,9 @@ class TablesInfo(C.Structure):
         ("lut_big_entries", C.c_int32),
         ("lut_big_shift", C.c_int32),
         ("lut_big_unsafe_leaves", C.c_int32),
+        ("lut_huge_entries", C.c_int32),
+        ("lut_huge_shift", C.c_int32),
+        ("lut_huge_unsafe_leaves", C.c_int32),
     ]
 
 

@@ -98,6 +98,7 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
       {t.ccnt.data(), t.ccnt.size() * 4, 0},
       {t.nbr.data(), t.nbr.size() * 4, 0},
       {t.lut_big.lut.data(), t.lut_big.lut.size() * 4, 0},
+      {t.lut_huge.lut.data(), t.lut_huge.lut.size() * 4, 0},
   };
   size_t total = 0;
   for (auto& p : parts) {
@@ -163,6 +164,15 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
     v.lv_big.shift1 = t.lut_big.shift1;
     v.lv_big.sub0 = t.lut_big.n_level1;
     v.lv_big.lut = reinterpret_cast<const uint32_t*>(b + parts[19].off);
+  }
+  v.n_lut_huge = (int32_t)t.lut_huge.lut.size();
+  v.n_level1_huge = (int32_t)t.lut_huge.n_level1;
+  v.lv_huge = v.lv;
+  if (v.n_lut_huge) {
+    v.lv_huge.kbase = t.lut_huge.kbase;
+    v.lv_huge.shift1 = t.lut_huge.shift1;
+    v.lv_huge.sub0 = t.lut_huge.n_level1;
+    v.lv_huge.lut = reinterpret_cast<const uint32_t*>(b + parts[20].off);
   }
   t.devs.push_back(d);
   *out = &t.devs.back();
@@ -249,6 +259,9 @@ int cs_tables_get_info(const cs_tables* tp, cs_tables_info* o) {
   o->lut_big_entries = (int32_t)t.lut_big.lut.size();
   o->lut_big_shift = (int32_t)t.lut_big.shift1;
   o->lut_big_unsafe_leaves = (int32_t)t.lut_big.n_unsafe;
+  o->lut_huge_entries = (int32_t)t.lut_huge.lut.size();
+  o->lut_huge_shift = (int32_t)t.lut_huge.shift1;
+  o->lut_huge_unsafe_leaves = (int32_t)t.lut_huge.n_unsafe;
   return CS_OK;
 }
 
@@ -277,8 +290,8 @@ int cs_tables_lookup_host_lut(const cs_tables* tp, const void* caps, int64_t n, 
   if (!tp || (n > 0 && (!caps || !bins_out))) return fail(CS_E_INVALID, "null argument");
   const Tables& t = *reinterpret_cast<const Tables*>(tp);
   if (which == 0) return cs_tables_lookup_host(tp, caps, n, bins_out);
-  if (which != 1 || t.lut_big.lut.empty()) return fail(CS_E_INVALID, "no such LUT");
-  const Tables::Lut& L = t.lut_big;
+  const Tables::Lut& L = which == 2 ? t.lut_huge : t.lut_big;
+  if ((which != 1 && which != 2) || L.lut.empty()) return fail(CS_E_INVALID, "no such LUT");
   if (t.cap_dtype == CS_CAP_F32) {
     const uint32_t* c = reinterpret_cast<const uint32_t*>(caps);
     for (int64_t i = 0; i < n; ++i)

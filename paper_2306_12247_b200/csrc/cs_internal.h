@@ -102,6 +102,8 @@ struct DevTables {
   LutView lv;
   LutView lv_big;          // finer fp32 LUT for eval_kernel (n_lut_big == 0: none)
   int32_t n_lut_big, n_level1_big;
+  LutView lv_huge;         // finer still (many grids: thousands of thresholds; n_lut_huge == 0: none)
+  int32_t n_lut_huge, n_level1_huge;
   const uint64_t* vio;     // [U] lowest admissible cap bits per union bin (0 for bin 0)
   const uint64_t* sig;     // [M][U] segment ids of the 3 policies, 16 bits each
   const int32_t* seg_off;  // [M*3+1] offsets into seg
@@ -156,7 +158,7 @@ struct Tables {
     uint32_t shift1 = 0, n_level1 = 0, n_sub = 0, n_unsafe = 0;
     std::vector<uint32_t> lut;
   };
-  Lut lut_main, lut_big;
+  Lut lut_main, lut_big, lut_huge;
   // device copies (per device ordinal)
   struct Dev {
     int device = -1;

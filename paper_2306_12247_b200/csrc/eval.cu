@@ -126,6 +126,7 @@ struct EvalParams {
   // shared-memory layout (bytes)
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
   int32_t off_pkq, off_g_edge;  // PK: the 3 policies' quanta (CTA), block edges (per group)
+  int32_t gh_direct;  // long traces: fold each trace's histogram straight into hist (no CTA copy)
 };
 
 namespace {
@@ -576,7 +577,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
         count_switches(s_sig[(size_t)m * U + cb], s_sig[(size_t)m * U + pb], 0, 0, 0, sw_s, sw_dummy);
   };
   // union bins of one 16-B vector (4 caps) into b[] (LUT search only)
-  auto lut4 = [&](const uint4 raw, uint32_t (&b)[4], const unsigned vmask) {
+  auto lut4 = [&](const uint4 raw, uint32_t (&b)[4]) {
     const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
     uint32_t e[4];
 #pragma unroll
@@ -591,7 +592,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     // UNI (redirect-heavy tables: many multi-threshold buckets): a warp with any redirecting lane
     // runs only the redirect path (correct for plain leaves too) instead of both sides of a
     // divergent branch — C3 +3-6 %; with sparse redirects the per-lane branch is cheaper (C4)
-    const bool plain = UNI ? !__any_sync(vmask, (int32_t)any < 0) : (int32_t)any >= 0;
+    // (__activemask: the main loops' last iteration can be divergent)
+    const bool plain = UNI ? !__any_sync(__activemask(), (int32_t)any < 0) : (int32_t)any >= 0;
     if (plain) {  // no redirect (marker 0xFFF.....; leaves have bit 31 clear while U < 2^15)
       if (VIO) flags |= any;
 #pragma unroll
@@ -635,8 +637,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     }
   };
   // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
-  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4], const unsigned vmask = 0xffffffffu) {
-    lut4(raw, b, vmask);
+  auto bins4 = [&](const uint4 raw, int v, uint32_t (&b)[4]) {
+    lut4(raw, b);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
 #ifdef CS_DIAG_NO_ATOMS  // diagnostic build only: no histogram update (wrong aggregates)
@@ -688,7 +690,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     auto pass = [&](const uint4 raw, int v) {
       uint32_t b[4] = {0u, 0u, 0u, 0u};
       const bool act = v < ve;
-      if (act) bins4(raw, v, b, __activemask());
+      if (act) bins4(raw, v, b);
       const uint32_t left = __shfl_sync(0xffffffffu, b[3], (lane + 31) & 31);
       uint32_t pb = lane == 0 ? carry : left;
       carry = __shfl_sync(0xffffffffu, b[3], 31);
@@ -719,10 +721,9 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       pass(r, v);
     }
   } else {
-    // (full warps in the main loops: the redirect vote needs no __activemask)
-    auto vec4 = [&](const uint4 raw, int v, const unsigned vmask = 0xffffffffu) {
+    auto vec4 = [&](const uint4 raw, int v) {
       uint32_t b[4];
-      bins4(raw, v, b, vmask);
+      bins4(raw, v, b);
     };
     int v = gtid;
 #ifdef CS_TC
@@ -791,7 +792,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       vec4(r2, v + 2 * gsize);
       vec4(r3, v + 3 * gsize);
     }
-    for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v, __activemask());
+    for (; v < nvf; v += gsize) vec4(ldg_stream(vrow + (size_t)v * 16), v);
   }
   // tail (< 4 caps at the very end of a trace)
   for (int i = 4 * nvf + gtid; i < n; i += gsize) {
@@ -1275,7 +1276,8 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   uint32_t* s_ghist = reinterpret_cast<uint32_t*>(smem + P.off_ghist);
   uint32_t* s_gsteps = s_ghist + U;
   const bool want_hist = P.hist != nullptr && P.nseg == 1;
-  if (want_hist) {
+  const bool gh_direct = want_hist && P.gh_direct != 0;
+  if (want_hist && !gh_direct) {
     for (int i = threadIdx.x; i < U; i += blockDim.x) s_ghist[i] = 0u;
     if (threadIdx.x == 0) *s_gsteps = 0u;
   }
@@ -1393,7 +1395,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
       group_sync(gid_local, gsize);
     }
     if (P.nseg == 1) {
-      if (want_hist) {
+      if (want_hist && !gh_direct) {
         uint32_t before = 0;
         if (gtid == 0) before = atomicAdd(s_gsteps, (uint32_t)(s1e - s0));
         before = __shfl_sync(0xffffffffu, before, 0);
@@ -1408,7 +1410,14 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
         }
       }
       uint32_t* gh = want_hist ? s_ghist : (uint32_t*)nullptr;
-      if (!PEN && P.bin_epi)
+      if (gh_direct) {  // (the plan takes it only with the segment epilogues)
+        if (seg_staged)
+          finish_trace<PEN, false>(P, t, h, sw, vcnt, P.hist, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize,
+                                   gid_local);
+        else
+          finish_trace<PEN, true>(P, t, h, sw, vcnt, P.hist, P.seg_hdr, P.seg_idle,
+                                  reinterpret_cast<const double2*>(P.seg_val), scratch, gtid, gsize, gid_local);
+      } else if (!PEN && P.bin_epi)
         finish_trace_bins(P, t, h, vcnt, gh, s_binval, scratch, gtid, gsize, gid_local);
       else if (seg_staged)  // two instantiations so each reads its tables with a known address space
         finish_trace<PEN, false>(P, t, h, sw, vcnt, gh, s_seghdr, s_segidle, s_segval, scratch, gtid, gsize, gid_local);
@@ -1439,7 +1448,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     group_sync(gid_local, gsize);
   }
 
-  if (want_hist) {
+  if (want_hist && !gh_direct) {
     __syncthreads();
     for (int u = threadIdx.x; u < U; u += blockDim.x) {
       const uint32_t c = s_ghist[u];
@@ -1579,7 +1588,12 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     return "tables too large for shared memory (" + std::to_string(nsegs) +
            " selection segments: switch counters use 16-bit indices)";
   const size_t sig_bytes = pen ? a16((size_t)M * U * 8 + (size_t)(M * 3 + 1) * 4) : 0;
-  const size_t gh_bytes = a->hist ? a16((size_t)U * 4 + 4) : 0;
+  // long traces with the segment epilogue fold each trace's histogram straight into hist (U global
+  // atomics per trace are < 2 % of its steps) instead of keeping a CTA copy in shared memory
+  static const char* ghd_env = std::getenv("CS_PLAN_GH_DIRECT");  // tuning only
+  const bool gh_direct = a->hist != nullptr && !pk && !(M == 1 && !pen) &&
+                         (ghd_env ? std::atoi(ghd_env) != 0 : (int64_t)U * 64 <= a->n_steps);
+  const size_t gh_bytes = a->hist && !gh_direct ? a16((size_t)U * 4 + 4) : 0;
   // segment tables (prep_kernel): hdr [NS] u32, idle flags [M*3] i32, values [6][NS] f64 in the
   // workspace; the kernel stages hdr, flags and the 4 (6 with a penalty) value arrays it reads
   const size_t seg_hdr_b = (size_t)((nsegs + 3) & ~3) * 4, seg_idle_b = (size_t)((M * 3 + 3) & ~3) * 4;
@@ -1624,7 +1638,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
         for (int wpg : {1, 2, 4, 8, 16, 32}) {
           const int wpc = threads / 32;
           if (wpg > wpc) continue;
-          if (tiny ? wpg != wpc : wpg == 32) continue;  // tiny: one whole-CTA group per trace
+          if (tiny ? wpg != wpc : (wpg == 32 && force_wpg != 32)) continue;  // tiny: one whole-CTA group per trace
           // ... of at most 512 threads when the trace is too short to split (C1, 1440 steps:
           // 14.7 us per step at 512 threads, 16.8 at 1024 — staging and barriers dominate)
           // (unless the 3M + 1 per-group counters need the bigger CTA: > 170 grids)
@@ -1652,14 +1666,25 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     return b;
   };
   Cand c = search(lut_bytes);
-  bool big = false;
-  if (f32 && view.n_lut_big > 0 && !small && !std::getenv("CS_PLAN_NO_BIG")) {  // env: tuning only
-    const Cand cb = search(a16((size_t)view.n_lut_big * 4));
-    // ... and no bigger worker groups: a group's barriers and per-trace epilogue cost more than the
-    // finer LUT saves (C5: 8-warp groups with the big LUT 5.41 ms, 4-warp groups with the main 4.99)
-    if (cb.warps >= c.warps && cb.warps > 0 && cb.wpg <= c.wpg && (cb.staged || !c.staged)) c = cb, big = true;
+  int big = 0;  // 1: the big LUT, 2: the huge one
+  if (f32 && !small && !std::getenv("CS_PLAN_NO_BIG")) {  // env: tuning only
+    // a finer LUT when it costs no resident warps and no bigger worker groups: a group's barriers,
+    // shared histogram and per-trace epilogue cost more than the finer LUT saves (C5: 8-warp
+    // groups with the big LUT 5.41 ms, 4-warp groups with the main 4.99; C3: 16-warp groups with
+    // the shift-11 LUT 6.63 ms, 8-warp groups with the shift-12 5.86)
+    const Cand c0 = c;
+    for (int which : {2, 1}) {
+      const int32_t n = which == 2 ? view.n_lut_huge : view.n_lut_big;
+      if (n <= 0) continue;
+      const Cand cb = search(a16((size_t)n * 4));
+      if (cb.warps >= c0.warps && cb.warps > 0 && cb.wpg <= c0.wpg && (cb.staged || !c0.staged)) {
+        c = cb, big = which;
+        break;
+      }
+    }
   }
-  const size_t lut_b = big ? a16((size_t)view.n_lut_big * 4) : lut_bytes;  // the LUT staged
+  const int32_t n_lut_sel = big == 2 ? view.n_lut_huge : big == 1 ? view.n_lut_big : view.n_lut;
+  const size_t lut_b = a16((size_t)n_lut_sel * 4);  // the LUT staged
   const size_t fixed0 = lut_b + vio_bytes + sig_bytes + gh_bytes + pkq_bytes;
   int best_warps = c.warps, b_threads = c.threads, b_wpg = c.wpg, b_per_sm = c.per_sm;
   size_t b_smem = c.smem;
@@ -1694,9 +1719,9 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   EvalParams& P = pl.P;
   P = EvalParams{};
   P.tb = view;
-  P.lv = big ? view.lv_big : view.lv;
-  P.n_lut = big ? view.n_lut_big : view.n_lut;
-  P.n_level1 = big ? view.n_level1_big : view.n_level1;
+  P.lv = big == 2 ? view.lv_huge : big == 1 ? view.lv_big : view.lv;
+  P.n_lut = n_lut_sel;
+  P.n_level1 = big == 2 ? view.n_level1_huge : big == 1 ? view.n_level1_big : view.n_level1;
   {
     const uint32_t s1 = P.lv.shift1 < 32 ? P.lv.shift1 : 31, s2 = s1 >= 4 ? s1 - 4 : 0;
     P.lut_s2 = s2;
@@ -1728,6 +1753,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_sig = (int32_t)(lut_b + vio_bytes);
   P.off_ghist = (int32_t)(lut_b + vio_bytes + sig_bytes);
   P.off_pkq = (int32_t)(lut_b + vio_bytes + sig_bytes + gh_bytes);
+  P.gh_direct = gh_direct ? 1 : 0;
   P.off_seg = (int32_t)fixed0;
   P.seg_smem_bytes = b_staged ? (int32_t)seg_smem : 0;
   P.bin_epi = (bin_epi && b_staged) ? 1 : 0;  // only with its tables in shared memory

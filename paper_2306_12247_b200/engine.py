@@ -138,12 +138,13 @@ class Tables:
 
     def lookup_host(self, caps: np.ndarray, lut: str = "main") -> np.ndarray:
         """Host restatement of the device LUT search (test hook, not used by the product path).
-        ``lut="big"`` searches the finer fp32 LUT the evaluation kernel stages when it fits."""
+        ``lut="big"`` / ``"huge"`` search the finer fp32 LUTs the evaluation kernel stages when they
+        fit."""
         dt = np.float32 if self.cap_dtype == "f32" else np.float64
         caps = np.ascontiguousarray(caps, dtype=dt)
         out = np.zeros(caps.shape[0], dtype=np.int32)
         N.check(N.lib().cs_tables_lookup_host_lut(self._h, caps.ctypes.data, caps.shape[0],
-                                                  {"main": 0, "big": 1}[lut], out.ctypes.data))
+                                                  {"main": 0, "big": 1, "huge": 2}[lut], out.ctypes.data))
         return out
 
     # ---- evaluation ----

@@ -51,7 +51,7 @@ def test_lut_and_decode_match_reference(dtype):
         t = Tables.stage([grid], dtype, batching_mtl=case["batching_mtl"], multi_tenant_bs=case["multi_tenant_bs"])
         idx = [i for i, c in enumerate(case["caps"]) if dtype == "f64" or is_f32(c)]
         caps = np.array([case["caps"][i] for i in idx])
-        luts = ["main"] + (["big"] if t.info.lut_big_entries else [])
+        luts = ["main"] + (["big"] if t.info.lut_big_entries else []) + (["huge"] if t.info.lut_huge_entries else [])
         for lut in luts:
             ub = t.lookup_host(caps, lut)
             for p, regime in enumerate(REGIMES):
@@ -122,7 +122,25 @@ def test_lut_leaves_proven_violation_free():
         grid = grid_from_doc(case["grid"])
         t = Tables.stage([grid], "f32", batching_mtl=case["batching_mtl"], multi_tenant_bs=case["multi_tenant_bs"])
         assert t.info.lut_unsafe_leaves == 0 and t.info.lut_big_unsafe_leaves == 0, case["name"]
+        assert t.info.lut_huge_unsafe_leaves == 0, case["name"]
         assert t.info.n_segments >= 3
     g = synthesize_grid(SynthParams(mtl_cap=8, bs_cap=512, mem_model_mb=3072.0))
     info = Tables.stage([g], "f32").info
     assert info.lut_unsafe_leaves == 0 and info.lut_big_unsafe_leaves == 0
+
+
+def test_huge_lut_for_many_grids():
+    """Ten grids (thousands of union thresholds): the staging also builds the shift-11 'huge' LUT
+    that eval_kernel stages next to 8-warp groups; every LUT gives the same bins and is proven."""
+    import bench
+
+    t = Tables.stage(bench.make_grids("ten"), "f32")
+    info = t.info
+    assert info.lut_huge_entries > 0 and info.lut_huge_shift < info.lut_shift
+    assert info.lut_huge_unsafe_leaves == 0
+    rng = np.random.default_rng(5)
+    thr = np.array(sorted({p for g in bench.make_grids("ten") for p in g.columns()[4]}), np.float64)
+    caps = np.concatenate([rng.uniform(0, 360, 50000), thr, np.nextafter(thr, 0), np.nextafter(thr, 400),
+                           [0.0, -0.0, 1e30, np.inf]]).astype(np.float32)
+    ub = t.lookup_host(caps)
+    assert np.array_equal(t.lookup_host(caps, "huge"), ub)
