@@ -127,6 +127,7 @@ struct EvalParams {
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
   int32_t off_pkq, off_g_edge;  // PK: the 3 policies' quanta (CTA), block edges (per group)
   int32_t gh_direct;  // long traces: fold each trace's histogram straight into hist (no CTA copy)
+  int32_t off_g_ring;  // CS_TMA variant: per-warp bulk-copy rings (per group)
 };
 
 namespace {
@@ -137,6 +138,29 @@ __device__ __forceinline__ void group_sync(int gid_local, int gsize) {
   else
     asm volatile("bar.sync %0, %1;" ::"r"(1 + gid_local), "r"(gsize) : "memory");
 }
+
+#ifdef CS_TMA
+// ---- TMA-unit bulk copies (A/B variant CS_TMA=<stages>): cp.async.bulk global -> shared with an
+// mbarrier per stage, one 512-B pass (32 vectors) per copy ----
+constexpr int kTmaStages = CS_TMA;
+constexpr int kTmaStageBytes = 512;
+constexpr int kTmaWarpBytes = kTmaStages * (kTmaStageBytes + 8);
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "n"(kTmaStageBytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "n"(kTmaStageBytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+#endif
 
 // shared-memory counter += 1 (shared-window address)
 __device__ __forceinline__ void red_inc(uint32_t saddr) {
@@ -562,7 +586,7 @@ constexpr uint32_t kStepZero = 0xFFFFFFFFu;  // "no previous step" (never a bin)
 template <bool PEN, bool STEP, bool VIO, bool UNI>
 __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32& L, uint32_t* h, uint32_t* sw,
                                                 const uint64_t* s_sig, int64_t t, int64_t s0, int64_t s1e, int gtid,
-                                                int gsize) {
+                                                int gsize, uint32_t& tma_seq) {
   const int U = P.tb.U, M = P.tb.M;
   const uint32_t* row = reinterpret_cast<const uint32_t*>(P.caps) + t * P.ld;
   const unsigned char* vrow = reinterpret_cast<const unsigned char*>(row + s0);
@@ -726,6 +750,45 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       bins4(raw, v, b);
     };
     int v = gtid;
+#ifdef CS_TMA
+    if (!STEP) {
+      // each warp streams its passes (32 consecutive vectors, 512 B, every gsize vectors) through a
+      // kTmaStages-deep shared-memory ring filled by the TMA unit (lane 0 issues, all lanes wait on
+      // the stage's mbarrier, then read their 16 B with LDS.128)
+      const int lane = gtid & 31, wig = gtid >> 5;
+      unsigned char* ring = reinterpret_cast<unsigned char*>(h) + P.off_g_ring + wig * kTmaWarpBytes;
+      const uint32_t rs = (uint32_t)__cvta_generic_to_shared(ring);
+      const uint32_t bs = rs + kTmaStages * kTmaStageBytes;
+      const int first = wig * 32;
+      const int npass = nvf >= first + 32 ? (nvf - first - 32) / gsize + 1 : 0;
+      // (the barriers are initialised once per kernel; tma_seq counts this warp's stage uses
+      // across traces, so stage = seq % stages and the phase parity = (seq / stages) & 1)
+      if (npass > 0) {
+        const uint32_t q0 = tma_seq;
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          for (int k = 0; k < kTmaStages && k < npass; ++k) {
+            const uint32_t st = (q0 + k) % kTmaStages;
+            bulk_load(rs + st * kTmaStageBytes, vrow + (size_t)(first + k * gsize) * 16, bs + 8 * st);
+          }
+        }
+        __syncwarp();
+        for (int p = 0; p < npass; ++p) {
+          const uint32_t q = q0 + p, st = q % kTmaStages;
+          mbar_wait(bs + 8 * st, (q / kTmaStages) & 1u);
+          const uint4 raw = *reinterpret_cast<const uint4*>(ring + st * kTmaStageBytes + lane * 16);
+          vec4(raw, first + p * gsize + lane);
+          __syncwarp();
+          if (lane == 0 && p + kTmaStages < npass) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(rs + st * kTmaStageBytes, vrow + (size_t)(first + (p + kTmaStages) * gsize) * 16, bs + 8 * st);
+          }
+        }
+        tma_seq = q0 + npass;
+      }
+      v = first + npass * gsize + lane;  // the remaining (partial) pass goes through the loops below
+    }
+#endif
 #ifdef CS_TC
     if (!STEP) {
       // time-clustered lanes: each warp instruction covers 32 CONSECUTIVE caps (4 coalesced 32-bit
@@ -1344,6 +1407,16 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
 
   const int64_t n_items = P.T * (int64_t)P.nseg;
   const int64_t n_groups = (int64_t)gridDim.x * P.gpc;
+  uint32_t tma_seq = 0;  // CS_TMA variant: this warp's bulk-copy stage uses so far
+#ifdef CS_TMA
+  if ((gtid & 31) == 0) {
+    const uint32_t bs = (uint32_t)__cvta_generic_to_shared(gbase + P.off_g_ring + (gtid >> 5) * kTmaWarpBytes) +
+                        kTmaStages * kTmaStageBytes;
+    for (int k = 0; k < kTmaStages; ++k) mbar_init(bs + 8 * k);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+#endif
   int iter = 0;
   for (int64_t item = (int64_t)blockIdx.x * P.gpc + gid_local; item < n_items; item += n_groups, ++iter) {
     if constexpr (PK) {  // whole traces (nseg == 1), two barriers per trace (pk_finish)
@@ -1384,7 +1457,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     const int64_t s1e = min(P.S, s0 + P.seg_len);
     bool bad;
     if constexpr (F32)
-      bad = run_segment_f32<PEN, STEP, VIO, UNI>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize);
+      bad = run_segment_f32<PEN, STEP, VIO, UNI>(P, L, h, sw, s_sig, t, s0, s1e, gtid, gsize, tma_seq);
     else
       bad = run_segment_f64<PEN, STEP, VIO>(P, L64, h, sw, s_sig, t, s0, s1e, gtid, gsize);
     if (VIO && bad) atomicOr(&vcnt[M * 3], 1u);
@@ -1613,6 +1686,14 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     *off_v = gb;
     gb += a16((size_t)(M * 3 + 4) * 4);  // PK: + alternating flag, block / scan-chunk counters
     if (pk) gb += a16((size_t)pk_nblk * 4);  // block edges (pk_main)
+#ifdef CS_TMA
+    gb = a16(gb);
+    *off_scr = gb;  // (the ring is placed by the kernel at off_g_ring = this + scratch)
+    gb += (size_t)wpg * (pk ? kPkScrWarp : 24) * 8;
+    gb = (gb + 127) & ~(size_t)127;
+    gb += (size_t)wpg * kTmaWarpBytes;
+    return a16(gb);
+#endif
     *off_scr = gb;
     gb += (size_t)wpg * (pk ? kPkScrWarp : 24) * 8;
     return a16(gb);
@@ -1769,6 +1850,9 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_g_vio = (int32_t)o2;
   P.off_g_scr = (int32_t)o3;
   P.off_g_edge = (int32_t)(o2 + a16((size_t)(M * 3 + 4) * 4));
+#ifdef CS_TMA
+  P.off_g_ring = (int32_t)((o3 + (size_t)pl.wpg * (pk ? kPkScrWarp : 24) * 8 + 127) & ~(size_t)127);
+#endif
   return std::string();
 }
 

@@ -6,6 +6,6 @@ for c in $CFGS; do
   IFS=: read name T kind <<< "$c"
   for v in base $V; do
     L=paper_2306_12247_b200/_lib/libcapsim_b200.so; [ $v != base ] && L=paper_2306_12247_b200/_lib/libcapsim_b200_$v.so
-    echo "$v $(CAPSIM_B200_LIB=$L python tools/diag_config.py $name $T $kind | cut -c1-90)"
+    echo "$v $(CAPSIM_B200_LIB=$L timeout 300 python tools/diag_config.py $name $T $kind | cut -c1-90)"
   done
 done
