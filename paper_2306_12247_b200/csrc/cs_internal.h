@@ -25,25 +25,29 @@ namespace cs {
 // IEEE floats order like their bit patterns, so the search runs on integer bits.
 //
 // fp32 (the streaming path):
-//   k  = clamp((int32)bits >> S1 - KBASE, 0, NB-1)   bucket; bucket 0 and NB-1 are empty guard
-//                                                    buckets, so -0.0 / tiny caps land in bin 0
-//                                                    and caps above every threshold (and NaN)
-//                                                    in the top bin
-//   e  = lut[k]
-//   while e >= 0xFFF00000 (redirect): s = e & 31; e = lut[SUB0 + ((e >> 5) & 0x7FFF)*16 + ((bits >> s) & 15)]
-//   b  = (e + ((bits & mask(s)) << 2)) >> 16          mask(s) = (2^s - 1) & 0x3FFF
-// Leaf encoding: hi16 = base bin (thresholds below the bucket), lo16 = K where K = 0 when no
-// threshold lies in the bucket (or it sits on the bucket start: base is then +1), else
-// K = (0x4000 - (T - bucket_start)) << 2, so adding the cap's low bits carries into bit 16
-// exactly when T <= cap. One LEA + one SHF per cap. Bit 0 (K is a multiple of 4) marks a leaf
-// that is NOT proven violation-free (selected power <= every cap it serves): the kernel's
-// per-step power check is an OR of that bit, with an exact recount when it is ever set.
+//   x  = clamp((int32)bits, LO, HI)                   LO = KBASE << S1, HI = ((KBASE + NB) << S1) - 1:
+//                                                    bucket 0 and NB-1 are empty guard buckets, so
+//                                                    -0.0 / negatives / tiny caps land in bin 0 and
+//                                                    caps above every threshold (and NaN) in the top bin
+//   e  = lut[(x >> S1) - KBASE]
+//   while e & 2 (redirect): s = (e >> 2) & 31; e = lut[SUB0 + (e >> 7)*16 + ((x >> s) & 15)]
+//   b  = (e + (x << 2)) >> 16                         one LEA + one PRMT per cap
+// Leaf encoding (S <= 14 for every fp32 bucket): with the bucket [start, start + 2^S), a leaf
+// holds E - (start << 2) mod 2^32 where E's hi16 = base bin (thresholds below the bucket) and
+// lo16 = K: K = 0 when no threshold lies in the bucket (or it sits on the bucket start: base is
+// then +1), else K = (0x4000 - (T - start)) << 2 — so e + (x << 2) = E + ((x - start) << 2)
+// carries into bit 16 exactly when T <= cap, and no mask of the cap's low bits is needed (the
+// clamp keeps x inside its bucket). Bit 0 (K is a multiple of 4) marks a leaf that is NOT proven
+// violation-free (selected power <= every cap it serves): the kernel's per-step power check is
+// an OR of that bit, with an exact recount when it is ever set. Bit 1 marks a redirect:
+// (sub-table id << 7) | (S' << 2) | 2, the sub-table splitting its bucket 16 ways at S' = S - 4.
 //
 // fp64 (drop-in PowerTrace values): u = clamp(bits, LO, HI); level-1 = (u >> S1) - KBASE;
 // leaf hi16 = base, bit 0 = n in {0, 1}, bit 14 = not proven violation-free; b = base +
 // (n && T64[base] <= u); redirect = 0x8000|s with hi16 = sub-table index.
 // ---------------------------------------------------------------------------------------
-constexpr uint32_t kRedirect32 = 0xFFF00000u;  // fp32 redirect marker (top 12 bits set; leaf bases < 0xFFF0)
+constexpr uint32_t kRedirect32 = 2u;  // fp32 redirect flag bit (leaves keep bit 1 clear)
+constexpr uint32_t kMaxShift32 = 14;  // fp32 bucket shifts (the leaf's K has 14 bits)
 constexpr uint32_t kRedirect = 0x8000u;        // fp64 redirect flag
 constexpr int kSubFan = 16;
 constexpr uint32_t kMaxSub32 = 32768;  // 15-bit sub-table id in an fp32 redirect entry
@@ -58,16 +62,14 @@ struct LutView {
 };
 
 CS_HD uint32_t bin_f32(uint32_t bits, uint32_t s1, int32_t kbase, int32_t nb, uint32_t sub0, const uint32_t* lut) {
-  int32_t k = ((int32_t)bits >> s1) - kbase;
-  k = k < 0 ? 0 : k;
-  k = k > nb - 1 ? nb - 1 : k;
-  uint32_t e = lut[k];
-  uint32_t s = s1;
-  while (e >= kRedirect32) {
-    s = e & 31u;
-    e = lut[sub0 + ((e >> 5) & 0x7FFFu) * kSubFan + ((bits >> s) & 15u)];
-  }
-  return (e + ((bits & ((1u << s) - 1u) & 0x3FFFu) << 2)) >> 16;
+  const int32_t lo = kbase << s1, hi = ((kbase + nb) << s1) - 1;
+  int32_t xi = (int32_t)bits;
+  xi = xi < lo ? lo : xi;
+  xi = xi > hi ? hi : xi;
+  const uint32_t x = (uint32_t)xi;
+  uint32_t e = lut[(xi >> s1) - kbase];
+  while (e & kRedirect32) e = lut[sub0 + (e >> 7) * kSubFan + ((x >> ((e >> 2) & 31u)) & 15u)];
+  return (e + (x << 2)) >> 16;
 }
 
 CS_HD uint32_t bin_f64(uint64_t bits, int64_t lo, int64_t hi, uint32_t s1, uint64_t kbase, uint32_t sub0,

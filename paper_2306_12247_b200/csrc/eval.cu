@@ -119,8 +119,8 @@ struct EvalParams {
   double omp;
   int32_t wpg, gpc;
   // fp32 LUT constants of the redirect step derived on the host (kernel-parameter operands,
-  // never rematerialised in the loop): shift and leaf mask one level down (s1 - 4)
-  uint32_t lut_s2, lut_mask2;
+  // never rematerialised in the loop): the shift one level down (s1 - 4)
+  uint32_t lut_s2;
   // fp32 bits of the lowest union threshold: caps below it are union bin 0 (idle everywhere)
   int32_t t0_bits;
   // shared-memory layout (bytes)
@@ -544,38 +544,34 @@ __device__ void recount_violations(const EvalParams& P, const uint32_t* s_lut, c
 // fp32 LUT search with its constants held in registers (encoding: cs_internal.h).
 struct Lut32 {
   const uint32_t* lut;  // shared
-  int32_t kb, nbm1;
-  uint32_t s1, sub0, mask1;
-  uint32_t s2, mask2;  // shift and leaf mask one level down (s1 - 4)
+  int32_t lo, hi, kb;   // clamp range of the cap bits (guard buckets included), level-1 offset
+  uint32_t s1, s2, sub0;  // level-1 shift, the shift one level down (s1 - 4), first sub-table entry
 
-  // level-1 entry: the bucket index is clamped into [0, NB-1]; buckets 0 and NB-1 are empty
-  // guards, so -0.0 / negatives land in bin 0 and caps above every threshold in the top bin
-  __device__ __forceinline__ uint32_t entry(uint32_t x) const {
-    int32_t k = ((int32_t)x >> s1) - kb;
-    k = min(max(k, 0), nbm1);
-    return lut[k];
+  // the clamp keeps every cap inside its bucket (buckets 0 and NB-1 are empty guards: -0.0 /
+  // negatives land in bin 0, caps above every threshold and NaN in the top bin), so a leaf needs
+  // no mask of the cap's low bits
+  __device__ __forceinline__ uint32_t clampx(uint32_t x) const { return (uint32_t)min(max((int32_t)x, lo), hi); }
+  __device__ __forceinline__ uint32_t entry(uint32_t xc) const { return lut[((int32_t)xc >> s1) - kb]; }
+  __device__ __forceinline__ static uint32_t leaf(uint32_t e, uint32_t xc) {
+    // e + (cap << 2) carries into bit 16 iff the bucket's threshold <= cap (one LEA); the high
+    // half is taken with PRMT so the histogram address becomes one more LEA (bin * 4 + base)
+    return __byte_perm(e + (xc << 2), 0u, 0x4432);
   }
-  __device__ __forceinline__ static uint32_t leaf(uint32_t e, uint32_t x, uint32_t mask) {
-    // (e + (low bits << 2)) carries into bit 16 iff the bucket's threshold <= cap; the high half
-    // is taken with PRMT so the histogram address becomes one LEA (bin * 4 + base) instead of the
-    // SHF + LOP3 + IADD the compiler otherwise folds (>> 16) * 4 into
-    return __byte_perm(e + ((x & mask) << 2), 0u, 0x4432);
+  __device__ __forceinline__ uint32_t sub(uint32_t e, uint32_t xc, uint32_t s) const {
+    return lut[sub0 + (e >> 7) * kSubFan + ((xc >> s) & 15u)];
   }
   // resolve through redirect sub-tables; ORs the final leaf's "unproven" bit into flags
-  __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t x, uint32_t& flags) const {
-    uint32_t s = s1;
-    while (e >= kRedirect32) {
-      s = e & 31u;
-      e = lut[sub0 + ((e >> 5) & 0x7FFFu) * kSubFan + ((x >> s) & 15u)];
-    }
+  __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t xc, uint32_t& flags) const {
+    while (e & kRedirect32) e = sub(e, xc, (e >> 2) & 31u);
     flags |= e;
-    return leaf(e, x, ((1u << s) - 1u) & 0x3FFFu);
+    return leaf(e, xc);
   }
   __device__ __forceinline__ uint32_t bin(uint32_t x, uint32_t& flags) const {
-    const uint32_t e = entry(x);
-    if (e >= kRedirect32) return deep(e, x, flags);
+    const uint32_t xc = clampx(x);
+    const uint32_t e = entry(xc);
+    if (e & kRedirect32) return deep(e, xc, flags);
     flags |= e;
-    return leaf(e, x, mask1);
+    return leaf(e, xc);
   }
 };
 
@@ -602,7 +598,7 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
   };
   // union bins of one 16-B vector (4 caps) into b[] (LUT search only)
   auto lut4 = [&](const uint4 raw, uint32_t (&b)[4]) {
-    const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+    const uint32_t u[4] = {L.clampx(raw.x), L.clampx(raw.y), L.clampx(raw.z), L.clampx(raw.w)};
     uint32_t e[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -617,47 +613,37 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
     // runs only the redirect path (correct for plain leaves too) instead of both sides of a
     // divergent branch — C3 +3-6 %; with sparse redirects the per-lane branch is cheaper (C4)
     // (__activemask: the main loops' last iteration can be divergent)
-    const bool plain = UNI ? !__any_sync(__activemask(), (int32_t)any < 0) : (int32_t)any >= 0;
-    if (plain) {  // no redirect (marker 0xFFF.....; leaves have bit 31 clear while U < 2^15)
+    const bool plain = UNI ? !__any_sync(__activemask(), (any & kRedirect32) != 0u) : (any & kRedirect32) == 0u;
+    if (plain) {
       if (VIO) flags |= any;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
-    } else {  // redirects (or, for >= 2^15 bins, high bases)
-      // one predicated sub-table step per element — a level-1 redirect always splits its bucket
-      // at shift s1 - 4 (staging.cpp: LutBuilder::make), so shift and leaf mask are constants —
-      // then the general loop only for chains (rare)
-      uint32_t msk[4];
+      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k]);
+    } else {
+      // one sub-table step per element — a level-1 redirect always splits its bucket at shift
+      // s1 - 4 (staging.cpp: LutBuilder::make), so the shift is a constant — then the general
+      // loop only for chains (rare)
       if (UNI) {  // branch-free: every element loads (non-redirects read entry 0, a broadcast;
                   // the predicated loads compiled to four divergent branches: C3 +2.4 %, iid +5.7 %)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const bool r = e[k] >= kRedirect32;
-          const uint32_t i = r ? L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> L.s2) & 15u) : 0u;
+          const bool r = (e[k] & kRedirect32) != 0u;
+          const uint32_t i = r ? L.sub0 + (e[k] >> 7) * kSubFan + ((u[k] >> L.s2) & 15u) : 0u;
           const uint32_t e2 = L.lut[i];
-          msk[k] = r ? L.mask2 : L.mask1;
           e[k] = r ? e2 : e[k];
         }
-      } else
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        msk[k] = L.mask1;
-        if (e[k] >= kRedirect32) {
-          msk[k] = L.mask2;
-          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> L.s2) & 15u)];
-        }
-      }
-      if (e[0] >= kRedirect32 || e[1] >= kRedirect32 || e[2] >= kRedirect32 || e[3] >= kRedirect32) {
+      } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          while (e[k] >= kRedirect32) {
-            const uint32_t sh = e[k] & 31u;
-            e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh) & 15u)];
-            msk[k] = ((1u << sh) - 1u) & 0x3FFFu;
-          }
+          if (e[k] & kRedirect32) e[k] = L.sub(e[k], u[k], L.s2);
+      }
+      if ((e[0] | e[1] | e[2] | e[3]) & kRedirect32) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          while (e[k] & kRedirect32) e[k] = L.sub(e[k], u[k], (e[k] >> 2) & 31u);
       }
       if (VIO) flags |= e[0] | e[1] | e[2] | e[3];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], msk[k]);
+      for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k]);
     }
   };
   // bins of one 16-B vector (4 caps) into b[], histogram atomics, per-step output
@@ -883,37 +869,27 @@ constexpr int kPkBlkVec = 32;  // vectors (4 caps each) per block: one 32-lane p
 
 // bins of 4 caps (no redirect-uniform variant), ORing the leaves into flags
 __device__ __forceinline__ void lut4_f32(const Lut32& L, const uint4 raw, uint32_t (&b)[4], uint32_t& flags) {
-  const uint32_t u[4] = {raw.x, raw.y, raw.z, raw.w};
+  const uint32_t u[4] = {L.clampx(raw.x), L.clampx(raw.y), L.clampx(raw.z), L.clampx(raw.w)};
   uint32_t e[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) e[k] = L.entry(u[k]);
   const uint32_t any = e[0] | e[1] | e[2] | e[3];
-  if ((int32_t)any >= 0) {
+  if ((any & kRedirect32) == 0u) {
     flags |= any;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], L.mask1);
+    for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k]);
   } else {
-    uint32_t msk[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      msk[k] = L.mask1;
-      if (e[k] >= kRedirect32) {
-        msk[k] = L.mask2;
-        e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> L.s2) & 15u)];
-      }
-    }
-    if (e[0] >= kRedirect32 || e[1] >= kRedirect32 || e[2] >= kRedirect32 || e[3] >= kRedirect32) {
+    for (int k = 0; k < 4; ++k)
+      if (e[k] & kRedirect32) e[k] = L.sub(e[k], u[k], L.s2);
+    if ((e[0] | e[1] | e[2] | e[3]) & kRedirect32) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        while (e[k] >= kRedirect32) {
-          const uint32_t sh = e[k] & 31u;
-          e[k] = L.lut[L.sub0 + ((e[k] >> 5) & 0x7FFFu) * kSubFan + ((u[k] >> sh) & 15u)];
-          msk[k] = ((1u << sh) - 1u) & 0x3FFFu;
-        }
+        while (e[k] & kRedirect32) e[k] = L.sub(e[k], u[k], (e[k] >> 2) & 31u);
     }
     flags |= e[0] | e[1] | e[2] | e[3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k], msk[k]);
+    for (int k = 0; k < 4; ++k) b[k] = Lut32::leaf(e[k], u[k]);
   }
 }
 
@@ -1398,12 +1374,11 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   Lut32 L;
   L.lut = s_lut;
   L.kb = (int32_t)P.lv.kbase;
-  L.nbm1 = P.n_level1 - 1;
   L.s1 = P.lv.shift1;
+  L.lo = L.kb << L.s1;
+  L.hi = ((L.kb + P.n_level1) << L.s1) - 1;
   L.sub0 = P.lv.sub0;
-  L.mask1 = ((1u << P.lv.shift1) - 1u) & 0x3FFFu;  // (a kernel-parameter copy measured 2 % slower on C4)
   L.s2 = P.lut_s2;
-  L.mask2 = P.lut_mask2;
 
   const int64_t n_items = P.T * (int64_t)P.nseg;
   const int64_t n_groups = (int64_t)gridDim.x * P.gpc;
@@ -1806,7 +1781,6 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   {
     const uint32_t s1 = P.lv.shift1 < 32 ? P.lv.shift1 : 31, s2 = s1 >= 4 ? s1 - 4 : 0;
     P.lut_s2 = s2;
-    P.lut_mask2 = ((1u << s2) - 1u) & 0x3FFFu;
     pl.uni = f32 && (double)(P.n_lut - P.n_level1) / kSubFan > 0.05 * (double)P.n_level1;
   }
   P.t0_bits = (f32 && !t.thresholds.empty()) ? (int32_t)(uint32_t)t.thresholds[0] : INT32_MIN;

@@ -102,12 +102,13 @@ struct LutBuilder {
     uint32_t base = lb(start);
     uint32_t stop = (s >= 63) ? (uint32_t)T.size() : lb(end);
     uint32_t n = stop - base;
-    if (f32) {
-      if (n == 0) return (base << 16) | flag(start, base, false, 0);
-      if (n == 1 && s <= 14) {
+    if (f32) {  // leaves hold E - (start << 2) (cs_internal.h): the kernel adds (cap << 2)
+      const uint32_t off = (uint32_t)start << 2;
+      if (n == 0) return ((base << 16) | flag(start, base, false, 0)) - off;
+      if (n == 1 && s <= kMaxShift32) {
         const uint32_t tl = (uint32_t)(T[base] - start);
-        if (tl == 0) return ((base + 1) << 16) | flag(start, base + 1, false, 0);  // threshold on the start
-        return (base << 16) | ((0x4000u - tl) << 2) | flag(start, base, true, T[base]);
+        if (tl == 0) return (((base + 1) << 16) | flag(start, base + 1, false, 0)) - off;  // threshold on the start
+        return ((base << 16) | ((0x4000u - tl) << 2) | flag(start, base, true, T[base])) - off;
       }
     } else {  // fp64: bit 14 marks a leaf not proven violation-free (the kernel ORs it)
       if (n == 0) return (base << 16) | (flag(start, base, false, 0) << 14);
@@ -124,11 +125,11 @@ struct LutBuilder {
       } else {
         uint64_t v = (start & ~15ull) | i;
         if (v >= start && v < end) ent = make(v, 0);
-        else ent = lb(v) << 16;  // unreachable slot (never indexed by a cap of this bucket)
+        else ent = (lb(v) << 16) - (f32 ? (uint32_t)v << 2 : 0u);  // unreachable slot (never indexed)
       }
       sub[off + i] = ent;
     }
-    if (f32) return kRedirect32 | (id << 5) | ns;
+    if (f32) return (id << 7) | (ns << 2) | kRedirect32;
     return (id << 16) | kRedirect | ns;
   }
 };
@@ -159,9 +160,11 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
   bool fits = false;
   std::vector<std::pair<uint32_t, size_t>> cand;  // (shift, total) of the valid shifts
   for (uint32_t s = 0; s + 1 < width; ++s) {
-    if (f32 && s > 30) break;
+    if (f32 && s > kMaxShift32) break;
     uint64_t kb, nb;
-    if (!range(s, &kb, &nb) || nb > level1_max) continue;
+    // fp32 buckets stop at shift 14 (the leaf's K): thresholds spread over more than ~16 octaves
+    // take a longer level 1 at shift 14 instead of a coarser one
+    if (!range(s, &kb, &nb) || (nb > level1_max && !(f32 && s == kMaxShift32 && cand.empty()))) continue;
     LutBuilder lbld(T, f32);
     for (uint64_t k = 0; k < nb; ++k) lbld.make((kb + k) << s, s);
     const size_t total = nb + lbld.sub.size();
