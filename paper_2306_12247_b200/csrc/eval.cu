@@ -736,6 +736,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       bins4(raw, v, b);
     };
     int v = gtid;
+    // (warp-contiguous chunks per group warp, so the warps do not update the same bins at the same
+    // time, measured: C3 -0.5 %, within noise; 16/32-warp groups stay 25-90 % slower either way)
 #ifdef CS_TMA
     if (!STEP) {
       // each warp streams its passes (32 consecutive vectors, 512 B, every gsize vectors) through a
