@@ -509,8 +509,9 @@ def run_engine(args, cfg, rank, world, local):
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
                          "traffic_source": (f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
-                                            f"{tr['kernel']} ({tr['source']}): {tr['dram_bytes_per_timestep']:.4f} "
-                                            "B/timestep x this launch's timesteps") if tr else None,
+                                            f"{tr.get('kernel', 'eval_kernel')} ({tr['source']}): "
+                                            f"{tr['dram_bytes_per_timestep']:.4f} B/timestep x this launch's "
+                                            "timesteps") if tr else None,
                          "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured"
                          else "fallback 6.65 TB/s (B200_PROFILING.md)",
                          "algorithmic_bytes_per_launch": bytes_per_launch,

@@ -1,7 +1,7 @@
 """Summarise an ncu report of eval_kernel into the numbers DESIGN.md / bench.py cite.
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep --traces 100000 --steps 10080 \
-        --out profiles/r01/ncu_eval_kernel.json [--traffic-key C4:mixed:1000000]
+        --out profiles/r01/ncu_eval_kernel.json [--traffic-key C4:mixed:f32]
 
 Writes a JSON summary (duration, DRAM bytes, throughput %, occupancy, issue, L1TEX/smem
 pipe utilisation, instructions per timestep, stall mix) and, with --traffic-key, records the
@@ -91,8 +91,8 @@ def main() -> None:
     if a.traffic_key and "dram_bytes_per_timestep" in summ:
         p = Path(__file__).resolve().parents[1] / "profiles" / "ncu_traffic.json"
         doc = json.loads(p.read_text()) if p.exists() else {}
-        doc[a.traffic_key.rsplit(":", 1)[0]] = {"dram_bytes_per_timestep": summ["dram_bytes_per_timestep"],
-                                                "source": a.out}
+        doc[a.traffic_key] = {"dram_bytes_per_timestep": summ["dram_bytes_per_timestep"], "source": a.out,
+                              "kernel": summ.get("kernel", "eval_kernel")}
         p.write_text(json.dumps(doc, indent=2) + "\n")
 
 
