@@ -57,45 +57,45 @@ __device__ __forceinline__ void add_fixed(unsigned long long (&l)[4], double x) 
   l[3] += hi >> 32;
 }
 
-// One block per slice of traces; rows (grid, policy) in an outer loop; per row every thread sums
-// its traces, then a warp + block reduction and CS_SWEEP_WORDS global atomics per block.
+// One warp per (row, slice of traces): lanes stride over the slice's traces, then a butterfly
+// reduction of the CS_SWEEP_WORDS words and one global atomic per nonzero word. Rows run in
+// parallel (a one-trace C2 sweep has 30 rows: a block walking them in turn took 39 us).
 __global__ void __launch_bounds__(256) sweep_totals_kernel(const cs_agg* __restrict__ agg, int64_t T, int rows,
-                                                           unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long red[8][CS_SWEEP_WORDS];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t per = (T + gridDim.x - 1) / gridDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * per, t1 = min(T, t0 + per);
-  for (int r = 0; r < rows; ++r) {
-    unsigned long long v[CS_SWEEP_WORDS];
+                                                           int slices, int store, unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= (int64_t)rows * slices) return;
+  const int r = (int)(wid % rows), sl = (int)(wid / rows);
+  const int64_t per = (T + slices - 1) / slices;
+  const int64_t t0 = (int64_t)sl * per, t1 = min(T, t0 + per);
+  unsigned long long v[CS_SWEEP_WORDS];
 #pragma unroll
-    for (int k = 0; k < CS_SWEEP_WORDS; ++k) v[k] = 0ull;
-    unsigned long long thr[4] = {0ull, 0ull, 0ull, 0ull}, en[4] = {0ull, 0ull, 0ull, 0ull};
-    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-      const cs_agg a = agg[t * rows + r];
-      v[0] += (unsigned long long)a.num_steps;
-      v[1] += (unsigned long long)a.idle_steps;
-      v[2] += (unsigned long long)a.switches;
-      v[3] += (unsigned long long)a.violations;
-      add_fixed(thr, a.avg_throughput_ips);
-      add_fixed(en, a.energy_proxy_wh);
-    }
+  for (int k = 0; k < CS_SWEEP_WORDS; ++k) v[k] = 0ull;
+  unsigned long long thr[4] = {0ull, 0ull, 0ull, 0ull}, en[4] = {0ull, 0ull, 0ull, 0ull};
+  for (int64_t t = t0 + lane; t < t1; t += 32) {
+    const cs_agg a = agg[t * rows + r];
+    v[0] += (unsigned long long)a.num_steps;
+    v[1] += (unsigned long long)a.idle_steps;
+    v[2] += (unsigned long long)a.switches;
+    v[3] += (unsigned long long)a.violations;
+    add_fixed(thr, a.avg_throughput_ips);
+    add_fixed(en, a.energy_proxy_wh);
+  }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[4 + k] = thr[k], v[8 + k] = en[k];
+  for (int k = 0; k < 4; ++k) v[4 + k] = thr[k], v[8 + k] = en[k];
 #pragma unroll
-    for (int k = 0; k < CS_SWEEP_WORDS; ++k) {
+  for (int k = 0; k < CS_SWEEP_WORDS; ++k) {
 #pragma unroll
-      for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-    }
-    if (lane == 0)
+    for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  if (lane < CS_SWEEP_WORDS) {
+    unsigned long long x = 0ull;
 #pragma unroll
-      for (int k = 0; k < CS_SWEEP_WORDS; ++k) red[w][k] = v[k];
-    __syncthreads();
-    if (threadIdx.x < CS_SWEEP_WORDS) {
-      unsigned long long s = 0ull;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
-      if (s) atomicAdd(out + (size_t)r * CS_SWEEP_WORDS + threadIdx.x, s);
-    }
-    __syncthreads();
+    for (int k = 0; k < CS_SWEEP_WORDS; ++k) x = lane == k ? v[k] : x;
+    if (store)  // one slice per row: the warp owns the row (no memset, no atomics)
+      out[(size_t)r * CS_SWEEP_WORDS + lane] = x;
+    else if (x)
+      atomicAdd(out + (size_t)r * CS_SWEEP_WORDS + lane, x);
   }
 }
 
@@ -103,12 +103,19 @@ __global__ void __launch_bounds__(256) sweep_totals_kernel(const cs_agg* __restr
 
 std::string launch_sweep_totals(const cs_agg* agg, int64_t T, int rows, uint64_t* out, bool accumulate, int sms,
                                 cudaStream_t st) {
-  if (!accumulate) CS_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)rows * CS_SWEEP_WORDS * 8, st));
-  if (T <= 0 || rows <= 0) return std::string();
-  // ~8 traces per thread per row: few enough atomics, enough blocks to stream the records
-  const int64_t want = (T + 2047) / 2048;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-  sweep_totals_kernel<<<blocks, 256, 0, st>>>(agg, T, rows, reinterpret_cast<unsigned long long*>(out));
+  if (rows <= 0) return std::string();
+  if (T <= 0) {
+    if (!accumulate) CS_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)rows * CS_SWEEP_WORDS * 8, st));
+    return std::string();
+  }
+  // ~8 traces per lane and slice: few enough atomics, enough warps to stream the records
+  const int64_t want = (T + 255) / 256;
+  const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(1, (int64_t)sms * 64 / rows)));
+  const int64_t warps = (int64_t)rows * slices;
+  const int store = (slices == 1 && !accumulate) ? 1 : 0;  // small sweeps (C1/C2): one launch, no memset
+  if (!store && !accumulate) CS_CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)rows * CS_SWEEP_WORDS * 8, st));
+  const int blocks = (int)((warps + 7) / 8);
+  sweep_totals_kernel<<<blocks, 256, 0, st>>>(agg, T, rows, slices, store, reinterpret_cast<unsigned long long*>(out));
   CS_CUDA_TRY(cudaGetLastError());
   return std::string();
 }

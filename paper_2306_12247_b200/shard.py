@@ -153,7 +153,9 @@ def sweep_words(tables, agg, *, out=None, accumulate: bool = False, stream=None)
 
     rows = tables.n_grids * 3
     if out is None:
-        out = torch.zeros((rows, N.CS_SWEEP_WORDS), dtype=torch.int64, device=agg.device)
+        # (zeroed by the call unless accumulating; a fill kernel here cost C1/C2 steps 2.5 us)
+        out = (torch.zeros if accumulate else torch.empty)((rows, N.CS_SWEEP_WORDS), dtype=torch.int64,
+                                                           device=agg.device)
     if agg.shape[0] and (not agg.is_contiguous() or tuple(agg.shape[1:]) != (tables.n_grids, 3, 6)):
         raise ValueError("agg must be a contiguous [T, M, 3, 6] EvalResult.agg tensor")
     with torch.cuda.device(agg.device):

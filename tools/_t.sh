@@ -1,4 +1,2 @@
-L=paper_2306_12247_b200/_lib/libcapsim_b200_wchunk.so
-for cfg in "11 0" "11 16" "10 16" "10 32" "11 32"; do set -- $cfg
-  E="CAPSIM_B200_LIB=$L CS_LUT_FORCE_SHIFT=$1"; [ $2 != 0 ] && E="$E CS_PLAN_WPG=$2"
-  echo "shift=$1 wpg=$2: $(env $E timeout 300 python tools/diag_config.py C3 10000 mixed | cut -c1-230)"; done
+timeout 600 python -m pytest tests/test_gpu_multi_rank.py tests/test_gpu_abi_hardening.py -q -x 2>&1 | tail -2
+for c in C1 C2; do timeout 300 python bench.py --config $c --no-cpu --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['config']['workload'], d['value'], d['ms_per_step'], d['gpu_launches'])"; done
