@@ -543,15 +543,21 @@ __device__ void recount_violations(const EvalParams& P, const uint32_t* s_lut, c
 
 // fp32 LUT search with its constants held in registers (encoding: cs_internal.h).
 struct Lut32 {
-  const uint32_t* lut;  // shared
-  int32_t lo, hi, kb;   // clamp range of the cap bits (guard buckets included), level-1 offset
+  const uint32_t* lut;   // shared
+  uint32_t lutk;         // shared-window address of lut[-KBASE]: the bucket load is one SHF + LEA
+                         // (through inline PTX, or the compiler re-derives lut + (k - KBASE))
+  int32_t lo, hi, kb;    // clamp range of the cap bits (guard buckets included), level-1 offset
   uint32_t s1, s2, sub0;  // level-1 shift, the shift one level down (s1 - 4), first sub-table entry
 
   // the clamp keeps every cap inside its bucket (buckets 0 and NB-1 are empty guards: -0.0 /
   // negatives land in bin 0, caps above every threshold and NaN in the top bin), so a leaf needs
   // no mask of the cap's low bits
   __device__ __forceinline__ uint32_t clampx(uint32_t x) const { return (uint32_t)min(max((int32_t)x, lo), hi); }
-  __device__ __forceinline__ uint32_t entry(uint32_t xc) const { return lut[((int32_t)xc >> s1) - kb]; }
+  __device__ __forceinline__ uint32_t entry(uint32_t xc) const {
+    uint32_t e;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(lutk + ((uint32_t)((int32_t)xc >> s1) << 2)));
+    return e;
+  }
   __device__ __forceinline__ static uint32_t leaf(uint32_t e, uint32_t xc) {
     // e + (cap << 2) carries into bit 16 iff the bucket's threshold <= cap (one LEA); the high
     // half is taken with PRMT so the histogram address becomes one more LEA (bin * 4 + base)
@@ -1378,6 +1384,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   L.kb = (int32_t)P.lv.kbase;
   L.s1 = P.lv.shift1;
   L.lo = L.kb << L.s1;
+  L.lutk = (uint32_t)__cvta_generic_to_shared(s_lut) - 4u * (uint32_t)L.kb;
   L.hi = ((L.kb + P.n_level1) << L.s1) - 1;
   L.sub0 = P.lv.sub0;
   L.s2 = P.lut_s2;
