@@ -1,2 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_multi_rank.py tests/test_gpu_abi_hardening.py -q -x 2>&1 | tail -2
-for c in C1 C2; do timeout 300 python bench.py --config $c --no-cpu --no-e2e | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['config']['workload'], d['value'], d['ms_per_step'], d['gpu_launches'])"; done
+mkdir -p gpurun_out/san
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_small.py > gpurun_out/san/san_$tool.log 2>&1; echo "$tool rc=$?" >> gpurun_out/san/summary.txt
+done
+timeout 600 python tools/run_reference_tests.py -q > gpurun_out/san/reference_suite.log 2>&1; echo "refsuite rc=$?" >> gpurun_out/san/summary.txt

@@ -39,6 +39,13 @@ cs.Tables.stage([fine], "f64").evaluate(fc[:600].double(), 256, step_seconds=60,
 # ten grids (5,055 union thresholds): the warp-uniform redirect variant
 import bench  # noqa: E402
 
+# ten grids, long traces (>= 4M timesteps, >= 64 steps per union bin): the huge LUT staged next to
+# 8-warp groups, each trace's histogram folded straight into global memory
+tten = cs.Tables.stage(bench.make_grids("ten"), "f32")
+lt = cs.generate_traces(7, 604800, step_seconds=1, kind="mixed", seed=8)
+tten.evaluate(lt, 604800, step_seconds=1)
+assert tten.last_plan()["lut_shift"] == tten.info.lut_huge_shift, tten.last_plan()
+
 cs.Tables.stage(bench.make_grids("ten"), "f32").evaluate(caps, 2000, step_seconds=60)
 t64 = cs.Tables.stage([g], "f64")
 t64.evaluate(caps.double(), 2000, step_seconds=60, switch_penalty_s=5.0)
