@@ -173,6 +173,20 @@ int cs_eval_last_plan(cs_eval_plan* out);
 int cs_sweep_totals(const cs_agg* agg_dev, int64_t n_traces, int32_t n_rows, uint64_t* totals_dev, uint32_t flags,
                     void* stream);
 
+/* ---- single-process multi-GPU reduction of a sharded sweep (the
+ *      survey's cs_nccl_init / cs_reduce / cs_nccl_destroy; north star (4): "a single NCCL reduce over
+ *      NVLink for the aggregate statistics"). One NCCL communicator over this process's devices
+ *      (ncclCommInitAll) and one grouped int64 SUM all-reduce, in place, of one buffer per device —
+ *      the [union-bin histogram | cs_sweep_totals words] of that device's shard. NCCL is resolved at
+ *      run time (libnccl.so.2); without it these return CS_E_UNSUPPORTED. The reference has no
+ *      multi-GPU path: its sweeps are Python loops over (trace, grid, policy) (sim.py:130-188). ---- */
+typedef struct cs_comm cs_comm;
+int cs_comm_init_all(int32_t n_devices, const int32_t* devices, cs_comm** out);
+int cs_comm_size(const cs_comm* c, int32_t* n_devices);
+/* bufs[i] / streams[i] (nullable: default stream) belong to devices[i] of cs_comm_init_all */
+int cs_comm_allreduce_i64(cs_comm* c, int64_t* const* bufs, int64_t count, void* const* streams);
+int cs_comm_destroy(cs_comm* c);
+
 /* ---- per-cap API: select_config (policy.py:172-188) and feasible_set (policy.py:151-169) as
  *      warp-per-query argmax (shuffle) / ballot kernels over the grid's raw entries ---- */
 int cs_select_caps(const cs_tables* t, int32_t grid, int32_t policy, const double* caps_dev, int64_t n,

@@ -38,7 +38,8 @@ from .columnar import (
     table_to_reports,
 )
 from .engine import EvalResult, HostEngine, Tables, generate_traces
-from .shard import ShardedResult, SweepTotals, evaluate_sharded, shard_range, sweep_words
+from .shard import (DeviceComm, MultiDeviceResult, ShardedResult, SweepTotals, evaluate_devices, evaluate_sharded,
+                    shard_range, sweep_words)
 from .errors import CapsimError, ParseError, ValidationError
 from .policy import (
     BATCHING,
@@ -115,7 +116,7 @@ __all__ = [
     "save_trace", "select_config", "select_configs", "select_sampling", "simulate", "simulate_many",
     "slice_report", "synthesize_grid", "trace_array", "trace_csv_text", "trace_stats",
     "Tables", "EvalResult", "HostEngine", "generate_traces", "TraceMatrix",
-    "ShardedResult", "SweepTotals", "evaluate_sharded", "shard_range", "sweep_words", "load_traces", "load_trace_matrix",
+    "ShardedResult", "SweepTotals", "evaluate_sharded", "evaluate_devices", "DeviceComm", "MultiDeviceResult", "shard_range", "sweep_words", "load_traces", "load_trace_matrix",
     "ColumnarRun", "eval_table", "histogram_table", "load_columnar", "reports_table", "save_columnar", "steps_table",
     "table_to_reports",
     "REACTIVE", "ControlEvent", "ControllerReport", "ControllerState", "ControlMode", "EventKind",

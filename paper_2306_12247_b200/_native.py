@@ -49,7 +49,7 @@ EXPORTS = (
     "cs_engine_create", "cs_engine_destroy", "cs_engine_eval_host",
     "cs_sweep_totals", "cs_replay", "cs_generate_traces", "cs_select_sampling", "cs_entries_aggregate",
     "cs_traces_parse_files", "cs_traces_parse_text", "cs_traces_info", "cs_traces_copy", "cs_traces_pack",
-    "cs_traces_destroy",
+    "cs_traces_destroy", "cs_comm_init_all", "cs_comm_size", "cs_comm_allreduce_i64", "cs_comm_destroy",
 )
 
 
@@ -173,6 +173,10 @@ def _declare(L: C.CDLL) -> None:
         "cs_feasible_caps": ([vp, i32, i32, vp, i64, vp, vp], C.c_int),
         "cs_engine_create": ([i32, i64, i64, i32, P(vp)], C.c_int),
         "cs_engine_destroy": ([vp], C.c_int),
+        "cs_comm_init_all": ([i32, vp, P(vp)], C.c_int),
+        "cs_comm_size": ([vp, P(i32)], C.c_int),
+        "cs_comm_allreduce_i64": ([vp, vp, i64, vp], C.c_int),
+        "cs_comm_destroy": ([vp], C.c_int),
         "cs_engine_eval_host": ([vp, vp, vp, i64, i64, i64, i32, dbl, u32, vp, vp, P(i64), P(i64)], C.c_int),
         "cs_generate_traces": ([vp, i64, i64, i64, i64, i32, i32, C.c_float, C.c_uint64, vp], C.c_int),
         "cs_replay": ([vp, i32, vp, i64, i64, i64, i32, i32, vp, dbl, vp, vp, i32, C.c_uint64, vp, vp, vp], C.c_int),

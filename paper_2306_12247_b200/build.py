@@ -20,7 +20,8 @@ LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libcapsim_b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["staging.cpp", "capi.cpp", "eval.cu", "aux_kernels.cu", "replay.cu", "sampling.cu", "sweep.cu", "ingest.cpp"]
+SOURCES = ["staging.cpp", "capi.cpp", "eval.cu", "aux_kernels.cu", "replay.cu", "sampling.cu", "sweep.cu", "ingest.cpp",
+           "comm.cpp"]
 HEADERS = ["cs_internal.h", "cs_mt.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -72,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
         objs.append(str(obj))
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart=static", "-o", str(tmp), *objs, "-lpthread"]
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart=static", "-o", str(tmp), *objs, "-lpthread", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

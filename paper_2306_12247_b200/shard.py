@@ -195,3 +195,88 @@ def evaluate_sharded(tables, caps, n_steps: int | None = None, *, step_seconds: 
     w = buf[U:].view(-1, N.CS_SWEEP_WORDS).cpu().numpy()
     names = tuple(getattr(g, "model_name", f"grid{i}") for i, g in enumerate(tables.grids))
     return ShardedResult(res, buf[:U] if hist is not None else None, SweepTotals(w, n_traces_total, names))
+
+
+# ---- one process, several GPUs: the sweep's reduction through the C ABI's NCCL communicator ----
+class DeviceComm:
+    """NCCL communicator over this process's devices (cs_comm_init_all: ncclCommInitAll), for
+    single-process multi-GPU sweeps. ``allreduce`` sums one int64 buffer per device in place, in
+    one grouped NCCL call."""
+
+    def __init__(self, devices):
+        import ctypes as C
+
+        self.devices = [int(d) for d in devices]
+        arr = (C.c_int32 * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        N.check(N.lib().cs_comm_init_all(len(self.devices), arr, C.byref(h)))
+        self._h = h
+
+    def allreduce(self, bufs, streams=None):
+        import ctypes as C
+
+        import torch
+
+        if len(bufs) != len(self.devices):
+            raise ValueError("one buffer per device")
+        n = bufs[0].numel()
+        for b, d in zip(bufs, self.devices):
+            if b.dtype != torch.int64 or not b.is_contiguous() or b.device != torch.device("cuda", d) or b.numel() != n:
+                raise ValueError("buffers must be contiguous int64 tensors of equal size, one on each device")
+        ptrs = (C.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+        if streams is None:
+            streams = [torch.cuda.current_stream(d) for d in self.devices]
+        sp = (C.c_void_p * len(bufs))(*[s.cuda_stream for s in streams])
+        N.check(N.lib().cs_comm_allreduce_i64(self._h, ptrs, n, sp))
+        return bufs
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().cs_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+@dataclass
+class MultiDeviceResult:
+    local: list            # per-device EvalResult (each device's own traces)
+    hist: object           # int64 [U] global union-bin histogram (on the first device), or None
+    totals: SweepTotals    # global per-(grid, policy) sweep statistics
+
+
+def evaluate_devices(tables, caps_per_device, n_steps: int | None = None, *, step_seconds: int,
+                     switch_penalty_s: float = 0.0, comm: DeviceComm | None = None, **kw) -> MultiDeviceResult:
+    """A sweep sharded over the GPUs of ONE process: ``caps_per_device[i]`` is device i's shard (a
+    [T_i, ld] tensor on that device, e.g. ``generate_traces(..., first_trace_id=lo_i)``). Each
+    device evaluates its shard on its current stream (kernels of all devices run concurrently),
+    then one grouped NCCL int64 SUM all-reduce of every device's [histogram | sweep totals]."""
+    import torch
+
+    devices = [c.device.index for c in caps_per_device]
+    own = comm is None
+    comm = comm or DeviceComm(devices)
+    try:
+        results, bufs = [], []
+        for caps in caps_per_device:
+            with torch.cuda.device(caps.device):
+                res = tables.evaluate(caps, n_steps, step_seconds=step_seconds, switch_penalty_s=switch_penalty_s,
+                                      **kw)
+                words = sweep_words(tables, res.agg)
+                hist = res.hist
+                bufs.append(torch.cat([hist.view(-1) if hist is not None else words.new_zeros(0), words.view(-1)]))
+                results.append(res)
+        comm.allreduce(bufs)
+        U = results[0].hist.numel() if results[0].hist is not None else 0
+        with torch.cuda.device(caps_per_device[0].device):
+            w = bufs[0][U:].view(-1, N.CS_SWEEP_WORDS).cpu().numpy()
+        names = tuple(getattr(g, "model_name", f"grid{i}") for i, g in enumerate(tables.grids))
+        n_total = sum(int(c.shape[0]) for c in caps_per_device)
+        return MultiDeviceResult(results, bufs[0][:U] if U else None, SweepTotals(w, n_total, names))
+    finally:
+        if own:
+            comm.close()

@@ -76,3 +76,21 @@ def test_staging_errors_are_validation_errors():
     h = ctypes.c_void_p()
     with pytest.raises(ValidationError, match="duplicate"):
         N.check(N.lib().cs_tables_create(d, 1, 0, 1, 1, ctypes.byref(h)), invalid=ValidationError)
+
+
+def test_comm_without_gpu_fails_cleanly():
+    """cs_comm_init_all on a host without a usable GPU / NCCL reports an error code, never crashes."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2306_12247_b200 import _native as N
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU host: covered by tests/test_gpu_multi_device.py")
+    h = C.c_void_p()
+    devs = (C.c_int32 * 1)(0)
+    rc = N.lib().cs_comm_init_all(1, devs, C.byref(h))
+    assert rc != 0 and not h.value
+    assert N.lib().cs_comm_init_all(0, devs, C.byref(h)) != 0
+    assert N.lib().cs_comm_destroy(None) == 0
