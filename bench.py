@@ -432,7 +432,7 @@ def run_engine(args, cfg, rank, world, local):
         pg.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
+    with ClockSampler(dev, float(os.environ.get("CAPSIM_CLOCK_PERIOD_MS", "2")) / 1e3) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             res, words, buf = step()
