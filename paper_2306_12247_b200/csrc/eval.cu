@@ -1084,26 +1084,31 @@ __device__ __forceinline__ void pk_finish(const EvalParams& P, int64_t t, uint32
   const uint32_t lt = (1u << lane) - 1u;
   int n = 0;
   uint32_t* ctr2 = vcnt + 6;  // 128-bin chunks are grabbed dynamically too (the first nw statically)
+  const uint32_t qs = (uint32_t)__cvta_generic_to_shared(q);  // queue base (shared window, kept in a register)
   for (int base = wig * 128; base < U;) {
     const int u = base + 4 * lane;
     uint4 w = make_uint4(0u, 0u, 0u, 0u);
     if (u < U) w = *reinterpret_cast<const uint4*>(h + u);  // h[U..U4) stay zero
-    const uint32_t m = (w.x ? 1u : 0u) | (w.y ? 2u : 0u) | (w.z ? 4u : 0u) | (w.w ? 8u : 0u);
-    const uint32_t c = __popc(m);
-    const uint32_t b0 = __ballot_sync(FULL, c & 1u), b1 = __ballot_sync(FULL, c & 2u),
-                   b2 = __ballot_sync(FULL, c & 4u);
-    int pos = n + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
-    if (m & 1u) q[pos++] = (uint16_t)u;
-    if (m & 2u) q[pos++] = (uint16_t)(u + 1);
-    if (m & 4u) q[pos++] = (uint16_t)(u + 2);
-    if (m & 8u) q[pos] = (uint16_t)(u + 3);
-    n += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
-    __syncwarp();
-    while (n >= 32) {
-      n -= 32;
-      bin(q[n + lane]);
+    if (__any_sync(FULL, (w.x | w.y | w.z | w.w) != 0u)) {  // (a quarter of C5's chunks are empty)
+      const uint32_t m = (w.x ? 1u : 0u) | (w.y ? 2u : 0u) | (w.z ? 4u : 0u) | (w.w ? 8u : 0u);
+      const uint32_t c = __popc(m);
+      const uint32_t b0 = __ballot_sync(FULL, c & 1u), b1 = __ballot_sync(FULL, c & 2u),
+                     b2 = __ballot_sync(FULL, c & 4u);
+      uint32_t pa = qs + 2u * (uint32_t)(n + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (m & (1u << k)) {
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(pa), "h"((unsigned short)(u + k)) : "memory");
+          pa += 2u;
+        }
+      n += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+      __syncwarp();
+      while (n >= 32) {
+        n -= 32;
+        bin(q[n + lane]);
+      }
+      __syncwarp();
     }
-    __syncwarp();
     uint32_t g = 0;
     if (lane == 0) g = atomicAdd(ctr2, 1u);
     base = 128 * ((int)__shfl_sync(FULL, g, 0) + nw);
