@@ -116,6 +116,38 @@ def test_c3_plan_ten_grids_staged(cs, torch, ten, kind, pen):
     _check_switches(res, caps_np, ten, step, pen, traces=(0, 1, T - 1))
 
 
+@pytest.mark.parametrize("kind", ["mixed", "iid"])
+def test_c3_plan_long_traces_huge_lut_direct_histogram(cs, torch, ten, kind):
+    """C3's own plan: week-long 1-s traces (>= 64 steps per union bin) fold each trace's histogram
+    straight into global memory, which makes room for the shift-11 'huge' LUT next to 8-warp
+    groups (UNI kernel), whole traces per group (>= 2 traces per group). Aggregates of a sample
+    of traces against the oracle; the global histogram against a per-step run of every trace."""
+    T, S, step = 1184, 5056 * 64, 1  # 3.8e8 timesteps
+    caps = cs.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306)
+    torch.cuda.synchronize()
+    tables = cs.Tables.stage(ten, "f32")
+    res = tables.evaluate(caps, S, step_seconds=step, check_violations=True)
+    torch.cuda.synchronize()
+    plan = tables.last_plan()
+    assert plan["lut_shift"] == tables.info.lut_huge_shift and plan["warps_per_group"] == 8, plan
+    assert plan["redirect_uniform"] == 1 and plan["trace_segments"] == 1, plan
+    from oracle import oracle
+
+    pick = [0, 1, 2, 591, 592, 1000, T - 2, T - 1]
+    avg, idle, en, _ = oracle.simulate_batch(_oracle_grids(ten), caps[pick, :S].cpu().numpy(), step, 0.0,
+                                             n_threads=16)
+    assert np.array_equal(res.idle_steps[pick].cpu().numpy(), idle)
+    assert np.allclose(res.avg_throughput_ips[pick].cpu().numpy(), avg, rtol=REL_TOL, atol=0)
+    assert np.allclose(res.energy_proxy_wh[pick].cpu().numpy(), en, rtol=REL_TOL, atol=0)
+    assert int(res.violations.sum()) == 0
+    ps = tables.evaluate(caps, S, step_seconds=step, per_step=True)
+    hist = np.zeros(tables.n_union_bins, np.int64)
+    for a in range(0, T, 128):  # bincount in slices (4e8 bins)
+        ub = ps.step_bins[a:a + 128, :S].cpu().numpy().view(np.uint16).astype(np.int64)
+        hist += np.bincount(ub.ravel(), minlength=tables.n_union_bins)
+    assert np.array_equal(res.hist.cpu().numpy(), hist)
+
+
 @pytest.mark.parametrize("pen", [0.0, 10.0])
 @pytest.mark.parametrize("T", [1, 2])
 def test_c2_plan_split_trace_finalize(cs, torch, ten, pen, T):
