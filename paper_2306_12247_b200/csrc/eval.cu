@@ -783,52 +783,8 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
       v = first + npass * gsize + lane;  // the remaining (partial) pass goes through the loops below
     }
 #endif
-#ifdef CS_TC
-    if (!STEP) {
-      // time-clustered lanes: each warp instruction covers 32 CONSECUTIVE caps (4 coalesced 32-bit
-      // loads per 128-cap window: lane l takes caps l, l + 32, l + 64, l + 96), so slowly varying
-      // caps hit fewer distinct LUT entries / histogram bins per instruction
-      const int lane = gtid & 31;
-      const uint32_t* crow = reinterpret_cast<const uint32_t*>(vrow);
-      for (; v + 3 * gsize < nvf; v += 4 * gsize) {
-        uint4 r[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t* w = crow + 4 * (size_t)(v - lane + i * gsize) + lane;
-          r[i].x = __ldg(w);
-          r[i].y = __ldg(w + 32);
-          r[i].z = __ldg(w + 64);
-          r[i].w = __ldg(w + 96);
-        }
-        vec4(r[0], v);
-        vec4(r[1], v + gsize);
-        vec4(r[2], v + 2 * gsize);
-        vec4(r[3], v + 3 * gsize);
-      }
-    }
-#endif
-#ifdef CS_ROLL
-    // rolling pipeline: each vector's register is reloaded with the next batch's vector as soon
-    // as it is consumed, so loads stay in flight while the batch computes
-    if (v + 3 * gsize < nvf) {
-      uint4 r0 = ldg_stream(vrow + (size_t)v * 16), r1 = ldg_stream(vrow + (size_t)(v + gsize) * 16),
-            r2 = ldg_stream(vrow + (size_t)(v + 2 * gsize) * 16), r3 = ldg_stream(vrow + (size_t)(v + 3 * gsize) * 16);
-      for (;;) {
-        const int vn = v + 4 * gsize;
-        const bool more = vn + 3 * gsize < nvf;
-        vec4(r0, v);
-        if (more) r0 = ldg_stream(vrow + (size_t)vn * 16);
-        vec4(r1, v + gsize);
-        if (more) r1 = ldg_stream(vrow + (size_t)(vn + gsize) * 16);
-        vec4(r2, v + 2 * gsize);
-        if (more) r2 = ldg_stream(vrow + (size_t)(vn + 2 * gsize) * 16);
-        vec4(r3, v + 3 * gsize);
-        if (more) r3 = ldg_stream(vrow + (size_t)(vn + 3 * gsize) * 16);
-        v = vn;
-        if (!more) break;
-      }
-    }
-#endif
+    // (tried and measured, not kept: time-clustered lanes — 32 consecutive caps per warp
+    // instruction via 32-bit loads, C4 -5 % / C3 -4 %; a rolling reload pipeline, C3 +-0)
     // each lane keeps 4 independent 128-bit loads in flight per pass
     for (; v + 3 * gsize < nvf; v += 4 * gsize) {
 #if CS_PF_DIST > 0
