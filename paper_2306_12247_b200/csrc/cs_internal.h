@@ -30,7 +30,7 @@ namespace cs {
 //                                                    -0.0 / negatives / tiny caps land in bin 0 and
 //                                                    caps above every threshold (and NaN) in the top bin
 //   e  = lut[(x >> S1) - KBASE]
-//   while e & 2 (redirect): s = (e >> 2) & 31; e = lut[SUB0 + (e >> 7)*16 + ((x >> s) & 15)]
+//   while e & 2 (redirect): s = (e >> 2) & 31; e = lut[(e >> 9) + ((x >> s) & 15)]
 //   b  = (e + (x << 2)) >> 16                         one LEA + one PRMT per cap
 // Leaf encoding (S <= 14 for every fp32 bucket): with the bucket [start, start + 2^S), a leaf
 // holds E - (start << 2) mod 2^32 where E's hi16 = base bin (thresholds below the bucket) and
@@ -40,7 +40,8 @@ namespace cs {
 // clamp keeps x inside its bucket). Bit 0 (K is a multiple of 4) marks a leaf that is NOT proven
 // violation-free (selected power <= every cap it serves): the kernel's per-step power check is
 // an OR of that bit, with an exact recount when it is ever set. Bit 1 marks a redirect:
-// (sub-table id << 7) | (S' << 2) | 2, the sub-table splitting its bucket 16 ways at S' = S - 4.
+// (byte offset of the sub-table in the LUT << 7) | (S' << 2) | 2, the sub-table splitting its
+// bucket 16 ways at S' = S - 4 (byte offsets: the kernel forms the entry's address with adds).
 //
 // fp64 (drop-in PowerTrace values): u = clamp(bits, LO, HI); level-1 = (u >> S1) - KBASE;
 // leaf hi16 = base, bit 0 = n in {0, 1}, bit 14 = not proven violation-free; b = base +
@@ -68,7 +69,7 @@ CS_HD uint32_t bin_f32(uint32_t bits, uint32_t s1, int32_t kbase, int32_t nb, ui
   xi = xi > hi ? hi : xi;
   const uint32_t x = (uint32_t)xi;
   uint32_t e = lut[(xi >> s1) - kbase];
-  while (e & kRedirect32) e = lut[sub0 + (e >> 7) * kSubFan + ((x >> ((e >> 2) & 31u)) & 15u)];
+  while (e & kRedirect32) e = lut[(e >> 9) + ((x >> ((e >> 2) & 31u)) & 15u)];  // (e >> 7: byte offset)
   return (e + (x << 2)) >> 16;
 }
 

@@ -548,6 +548,7 @@ struct Lut32 {
                          // (through inline PTX, or the compiler re-derives lut + (k - KBASE))
   int32_t lo, hi, kb;    // clamp range of the cap bits (guard buckets included), level-1 offset
   uint32_t s1, s2, sub0;  // level-1 shift, the shift one level down (s1 - 4), first sub-table entry
+  uint32_t lutb, s2m2;    // shared-window address of lut[0]; s2 - 2 (staging keeps s1 >= 6)
 
   // the clamp keeps every cap inside its bucket (buckets 0 and NB-1 are empty guards: -0.0 /
   // negatives land in bin 0, caps above every threshold and NaN in the top bin), so a leaf needs
@@ -563,8 +564,18 @@ struct Lut32 {
     // half is taken with PRMT so the histogram address becomes one more LEA (bin * 4 + base)
     return __byte_perm(e + (xc << 2), 0u, 0x4432);
   }
+  // redirect entries hold their sub-table's byte offset (<< 7): any level, shift s
   __device__ __forceinline__ uint32_t sub(uint32_t e, uint32_t xc, uint32_t s) const {
-    return lut[sub0 + (e >> 7) * kSubFan + ((xc >> s) & 15u)];
+    return lut[(e >> 9) + ((xc >> s) & 15u)];
+  }
+  // the first redirect level (constant shift s2): the entry's byte address from adds only
+  __device__ __forceinline__ uint32_t sub_addr(uint32_t e, uint32_t xc) const {
+    return lutb + (e >> 7) + ((xc >> s2m2) & 0x3Cu);
+  }
+  __device__ __forceinline__ static uint32_t lds(uint32_t addr) {
+    uint32_t r;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+    return r;
   }
   // resolve through redirect sub-tables; ORs the final leaf's "unproven" bit into flags
   __device__ __forceinline__ uint32_t deep(uint32_t e, uint32_t xc, uint32_t& flags) const {
@@ -633,14 +644,13 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const bool r = (e[k] & kRedirect32) != 0u;
-          const uint32_t i = r ? L.sub0 + (e[k] >> 7) * kSubFan + ((u[k] >> L.s2) & 15u) : 0u;
-          const uint32_t e2 = L.lut[i];
+          const uint32_t e2 = Lut32::lds(r ? L.sub_addr(e[k], u[k]) : L.lutb);
           e[k] = r ? e2 : e[k];
         }
       } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (e[k] & kRedirect32) e[k] = L.sub(e[k], u[k], L.s2);
+          if (e[k] & kRedirect32) e[k] = Lut32::lds(L.sub_addr(e[k], u[k]));
       }
       if ((e[0] | e[1] | e[2] | e[3]) & kRedirect32) {
 #pragma unroll
@@ -845,7 +855,7 @@ __device__ __forceinline__ void lut4_f32(const Lut32& L, const uint4 raw, uint32
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (e[k] & kRedirect32) e[k] = L.sub(e[k], u[k], L.s2);
+      if (e[k] & kRedirect32) e[k] = Lut32::lds(L.sub_addr(e[k], u[k]));
     if ((e[0] | e[1] | e[2] | e[3]) & kRedirect32) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -1349,6 +1359,8 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   L.hi = ((L.kb + P.n_level1) << L.s1) - 1;
   L.sub0 = P.lv.sub0;
   L.s2 = P.lut_s2;
+  L.lutb = (uint32_t)__cvta_generic_to_shared(s_lut);
+  L.s2m2 = L.s2 >= 2u ? L.s2 - 2u : 0u;
 
   const int64_t n_items = P.T * (int64_t)P.nseg;
   const int64_t n_groups = (int64_t)gridDim.x * P.gpc;

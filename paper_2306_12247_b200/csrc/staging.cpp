@@ -78,9 +78,11 @@ struct LutBuilder {
   std::vector<uint32_t> sub;  // sub-table entries (appended after level 1)
   uint32_t n_sub = 0;
   uint32_t unsafe = 0;        // fp32 leaves whose selections are not proven to fit their caps
+  uint32_t sub0 = 0;          // fp32: first sub-table entry (= level-1 size): redirects hold byte offsets
+  bool too_big = false;       // fp32: a sub-table beyond the 25-bit byte offset of a redirect
 
-  LutBuilder(const std::vector<uint64_t>& t, bool is_f32, const std::vector<uint64_t>* v = nullptr)
-      : T(t), f32(is_f32), vio(v) {}
+  LutBuilder(const std::vector<uint64_t>& t, bool is_f32, const std::vector<uint64_t>* v = nullptr, uint32_t s0 = 0)
+      : T(t), f32(is_f32), vio(v), sub0(s0) {}
 
   // Bit 0 of an fp32 leaf (free: K is a multiple of 4) flags a leaf for which some cap of its
   // range could select a config drawing more than the cap. Proof per leaf: every cap of the
@@ -129,7 +131,11 @@ struct LutBuilder {
       }
       sub[off + i] = ent;
     }
-    if (f32) return (id << 7) | (ns << 2) | kRedirect32;
+    if (f32) {  // the sub-table's byte offset in the LUT, so the kernel forms its address with adds
+      const uint64_t off = ((uint64_t)sub0 + (uint64_t)id * kSubFan) * 4u;
+      if (off >= (1ull << 25)) too_big = true;
+      return ((uint32_t)off << 7) | (ns << 2) | kRedirect32;
+    }
     return (id << 16) | kRedirect | ns;
   }
 };
@@ -159,13 +165,14 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
   size_t best_total = ~(size_t)0;
   bool fits = false;
   std::vector<std::pair<uint32_t, size_t>> cand;  // (shift, total) of the valid shifts
-  for (uint32_t s = 0; s + 1 < width; ++s) {
+  // (fp32 shifts start at 6: the kernel's first sub-table step shifts the cap by S1 - 6 >= 0)
+  for (uint32_t s = f32 ? 6u : 0u; s + 1 < width; ++s) {
     if (f32 && s > kMaxShift32) break;
     uint64_t kb, nb;
     // fp32 buckets stop at shift 14 (the leaf's K): thresholds spread over more than ~16 octaves
     // take a longer level 1 at shift 14 instead of a coarser one
     if (!range(s, &kb, &nb) || (nb > level1_max && !(f32 && s == kMaxShift32 && cand.empty()))) continue;
-    LutBuilder lbld(T, f32);
+    LutBuilder lbld(T, f32, nullptr, (uint32_t)nb);
     for (uint64_t k = 0; k < nb; ++k) lbld.make((kb + k) << s, s);
     const size_t total = nb + lbld.sub.size();
     if (f32 && lbld.n_sub > kMaxSub32) continue;
@@ -187,11 +194,11 @@ std::string build_lut(const Tables& t, const std::vector<uint64_t>& T, bool f32,
   const uint32_t s = best_s;
   uint64_t kb, nb;
   if (!range(s, &kb, &nb)) return "power thresholds too small for the fp32 LUT (need bits > 2^S1)";
-  LutBuilder lbld(T, f32, &t.vio);
+  LutBuilder lbld(T, f32, &t.vio, (uint32_t)nb);
   out.kbase = kb;
   std::vector<uint32_t> level1(nb);
   for (uint64_t k = 0; k < nb; ++k) level1[k] = lbld.make((kb + k) << s, s);
-  if (f32 && lbld.n_sub > kMaxSub32) return "threshold LUT needs more than 32768 sub-tables";
+  if (f32 && (lbld.n_sub > kMaxSub32 || lbld.too_big)) return "threshold LUT needs more than 32768 sub-tables";
   if (lbld.n_sub > 65535) return "threshold LUT needs more than 65535 sub-tables";
   out.shift1 = s;
   out.n_level1 = (uint32_t)nb;
