@@ -925,14 +925,16 @@ __device__ __forceinline__ bool pk_main(const EvalParams& P, const Lut32& L, uin
     } else {
       uint32_t b[4];
       lut4_f32(L, raw, b, flags);
-      const uint32_t left = __shfl_sync(FULL, b[3], (lane + 31) & 31);
-      const uint32_t pb = lane == 0 ? b[0] : left;
       last = __shfl_sync(FULL, b[3], 31);
       if (lane == 0) edges[blk] = b[0] | (last << 16);
       uint2 sg[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) sg[k] = s_sig2[b[k]];
-      const uint2 sp = pb == b[0] ? sg[0] : s_sig2[pb];
+      // the signature of the step before lane l's vector is lane l-1's sg[3] (that step's): two
+      // shuffles instead of another LDS.64 on the L1TEX-bound loop; lane 0 (block start) counts
+      // its first step unswitched
+      const uint32_t px = __shfl_sync(FULL, sg[3].x, (lane + 31) & 31), py = __shfl_sync(FULL, sg[3].y, (lane + 31) & 31);
+      const uint2 sp = lane == 0 ? sg[0] : make_uint2(px, py);
       pk_count(hA, hW, dummy, b[0], sg[0], sp);
       pk_count(hA, hW, dummy, b[1], sg[1], sg[0]);
       pk_count(hA, hW, dummy, b[2], sg[2], sg[1]);
