@@ -1549,12 +1549,14 @@ void* kptr() {
   return (void*)eval_kernel<CapT, PEN, STEP, VIO, UNI, PK>;
 }
 
-// uni: the warp-uniform redirect variant (fp32, no penalty, no per-step output only)
+// uni: the warp-uniform redirect variant (fp32, no penalty, no per-step output only; CS_UNI builds)
 // pk: the packed-penalty variant (fp32, one grid, penalty, no per-step output, < 2^16 steps)
 void* pick_kernel(bool f32, bool pen, bool step, bool vio, bool uni = false, bool pk = false) {
   if (pk && f32 && pen && !step)
     return vio ? kptr<float, true, false, true, false, true>() : kptr<float, true, false, false, false, true>();
+#ifdef CS_UNI
   if (uni && f32 && !pen && !step) return vio ? kptr<float, false, false, true, true>() : kptr<float, false, false, false, true>();
+#endif
 #define CS_K(A, B, C) \
   if (pen == A && step == B && vio == C) return f32 ? kptr<float, A, B, C>() : kptr<double, A, B, C>();
   CS_K(false, false, false)
@@ -1765,7 +1767,14 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   {
     const uint32_t s1 = P.lv.shift1 < 32 ? P.lv.shift1 : 31, s2 = s1 >= 4 ? s1 - 4 : 0;
     P.lut_s2 = s2;
+    // the warp-uniform redirect variant (UNI) served redirect-heavy tables (C3) while the per-lane
+    // redirect step compiled to divergent branches; with predicated sub-table loads the per-lane
+    // path is faster there too (C3 5.36 -> 5.31 ms, iid equal): UNI is an A/B build only now
+#ifdef CS_UNI
     pl.uni = f32 && (double)(P.n_lut - P.n_level1) / kSubFan > 0.05 * (double)P.n_level1;
+#else
+    pl.uni = false;
+#endif
   }
   P.t0_bits = (f32 && !t.thresholds.empty()) ? (int32_t)(uint32_t)t.thresholds[0] : INT32_MIN;
   P.caps = a->caps;

@@ -2,8 +2,8 @@
 
 * C3's plan: the ten bench grids (5,000+ union thresholds), >= 4M timesteps, no per-step output,
   enough traces that no trace is split -> the large-launch plan (finer LUT and segment tables
-  staged when they fit), multi-warp worker groups and (without a penalty) the warp-uniform
-  redirect kernel variant.
+  staged when they fit), multi-warp worker groups; with week-long traces the huge LUT and
+  histograms folded straight into global memory.
 * C2's plan: the ten grids over one or two long traces -> traces split across worker groups,
   partial histograms and the per-(trace, grid) finalize kernel (gridDim.y = M).
 
@@ -109,8 +109,6 @@ def test_c3_plan_ten_grids_staged(cs, torch, ten, kind, pen):
     plan = tables.last_plan()
     assert plan["trace_segments"] == 1, plan
     assert plan["warps_per_group"] > 1, plan
-    if pen == 0.0:
-        assert plan["redirect_uniform"] == 1, plan    # the UNI kernel C3 runs
     _check_aggs(res, caps_np, ten, step, pen)
     _check_hist_and_switches(res, tables, caps, S, step, pen)
     _check_switches(res, caps_np, ten, step, pen, traces=(0, 1, T - 1))
@@ -120,7 +118,7 @@ def test_c3_plan_ten_grids_staged(cs, torch, ten, kind, pen):
 def test_c3_plan_long_traces_huge_lut_direct_histogram(cs, torch, ten, kind):
     """C3's own plan: week-long 1-s traces (>= 64 steps per union bin) fold each trace's histogram
     straight into global memory, which makes room for the shift-11 'huge' LUT next to 8-warp
-    groups (UNI kernel), whole traces per group (>= 2 traces per group). Aggregates of a sample
+    groups, whole traces per group (>= 2 traces per group). Aggregates of a sample
     of traces against the oracle; the global histogram against a per-step run of every trace."""
     T, S, step = 1184, 5056 * 64, 1  # 3.8e8 timesteps
     caps = cs.generate_traces(T, S, step_seconds=step, kind=kind, seed=2306)
@@ -130,7 +128,7 @@ def test_c3_plan_long_traces_huge_lut_direct_histogram(cs, torch, ten, kind):
     torch.cuda.synchronize()
     plan = tables.last_plan()
     assert plan["lut_shift"] == tables.info.lut_huge_shift and plan["warps_per_group"] == 8, plan
-    assert plan["redirect_uniform"] == 1 and plan["trace_segments"] == 1, plan
+    assert plan["trace_segments"] == 1, plan
     from oracle import oracle
 
     pick = [0, 1, 2, 591, 592, 1000, T - 2, T - 1]

@@ -36,7 +36,7 @@ fc2 = cs.generate_traces(2400, 1203, step_seconds=60, kind="mixed", seed=7)
 tf.evaluate(fc2, 1203, step_seconds=60, switch_penalty_s=10.0, check_violations=True)
 assert tf.last_plan()["epilogue"] in (3, 4), tf.last_plan()
 cs.Tables.stage([fine], "f64").evaluate(fc[:600].double(), 256, step_seconds=60, switch_penalty_s=10.0)
-# ten grids (5,055 union thresholds): the warp-uniform redirect variant
+# ten grids (5,055 union thresholds): redirect-heavy LUT (per-lane predicated sub-table loads)
 import bench  # noqa: E402
 
 # ten grids, long traces (>= 4M timesteps, >= 64 steps per union bin): the huge LUT staged next to
