@@ -455,6 +455,86 @@ __device__ __forceinline__ void epilogue(const EvalParams& P, int64_t t, const u
   }
 }
 
+// Warp-owned variant of epilogue() for the main kernel: each (grid, policy) pair belongs to one
+// warp of the group, whose lanes stride over the pair's selection segments and whose lane 0
+// writes the record — no cross-warp combine, so no barriers between the pairs (the per-pair
+// combine through shared scratch cost two group barriers per grid: ~13 % of C3's warp time was
+// spent waiting at them). Same per-segment arithmetic as epilogue().
+template <bool PEN, bool COMPACT>
+__device__ __forceinline__ void epilogue_warps(const EvalParams& P, int64_t t, const uint32_t* C, const uint32_t* SW,
+                                               const uint32_t* vcnt, const uint32_t* shdr, const int32_t* sidle,
+                                               const double2* sval, int gtid, int gsize) {
+  const DevTables& tb = P.tb;
+  const int M = tb.M, NS = P.NSEG;
+  const int lane = gtid & 31, wig = gtid >> 5, nw = gsize >> 5;
+  const unsigned FULL = 0xffffffffu;
+  for (int mp = wig; mp < 3 * M; mp += nw) {
+    const int m = mp / 3;
+    const int k0 = __ldg(tb.seg_off + mp), k1 = __ldg(tb.seg_off + mp + 1);
+    const uint32_t* sw = PEN ? SW + k0 : nullptr;
+    const int kidle = sidle[mp] ? k0 : -1;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    uint32_t idle = 0, swc = 0;
+    double qt = 0.0, qit = 0.0, qe = 0.0, qie = 0.0;
+    if (COMPACT) qt = __ldg(P.seg_q + 4 * mp), qit = __ldg(P.seg_q + 4 * mp + 1), qe = __ldg(P.seg_q + 4 * mp + 2),
+                 qie = __ldg(P.seg_q + 4 * mp + 3);
+    auto seg = [&](int k) {
+      const uint32_t hd = shdr[k];
+      const uint32_t ulo = hd & 0xFFFFu, uhi = hd >> 16;
+      const uint32_t cnt = C[uhi] - (ulo ? C[ulo - 1] : 0u);
+      if (cnt == 0) return;
+      const double dc = (double)cnt;
+      double2 r = make_double2(0.0, 0.0);
+      if (COMPACT) r = __ldg(P.seg_raw + k);
+      const double2 ve = COMPACT ? split_q(r.y, qe, qie) : sval[NS + k];
+      a[2] = __fma_rn(dc, ve.x, a[2]);
+      a[3] = __fma_rn(dc, ve.y, a[3]);
+      uint32_t scnt = 0;
+      if (PEN) {
+        scnt = sw[k - k0];
+        swc += scnt;
+      }
+      if (k == kidle) {
+        idle += cnt;
+      } else {
+        const double dn = (double)(cnt - scnt);
+        const double2 vt = COMPACT ? split_q(r.x, qt, qit) : sval[k];
+        a[0] = __fma_rn(dn, vt.x, a[0]);
+        a[1] = __fma_rn(dn, vt.y, a[1]);
+        if (PEN && scnt) {
+          const double ds = (double)scnt;
+          const double2 vp = COMPACT ? split_q(__dmul_rn(r.x, P.omp), qt, qit) : sval[2 * NS + k];
+          a[0] = __fma_rn(ds, vp.x, a[0]);
+          a[1] = __fma_rn(ds, vp.y, a[1]);
+        }
+      }
+    };
+    int k = k0 + lane;
+    for (; k + 32 < k1; k += 64) {  // two segments per iteration: their load chains overlap
+      seg(k);
+      seg(k + 32);
+    }
+    if (k < k1) seg(k);
+    const double mine = xreduce4(a, lane);  // lane kLaneOf4[c] holds component c
+    const uint32_t id = __reduce_add_sync(FULL, idle), sc = __reduce_add_sync(FULL, swc);
+    const double c0 = __shfl_sync(FULL, mine, kLaneOf4[0]), c1 = __shfl_sync(FULL, mine, kLaneOf4[1]),
+                 c2 = __shfl_sync(FULL, mine, kLaneOf4[2]), c3 = __shfl_sync(FULL, mine, kLaneOf4[3]);
+    if (lane == 0 && P.agg) {
+      dd tsum{c0, 0.0}, esum{c2, 0.0};
+      dd_add2(tsum, c1, 0.0);
+      dd_add2(esum, c3, 0.0);
+      cs_agg r;
+      r.avg_throughput_ips = __ddiv_rn(__dadd_rn(tsum.hi, tsum.lo), (double)P.S);  // fsum(ips)/n
+      r.energy_proxy_wh = __dadd_rn(esum.hi, esum.lo);
+      r.idle_steps = id;
+      r.switches = PEN ? sc : 0u;
+      r.violations = vcnt ? vcnt[mp] : 0u;
+      r.num_steps = P.S;
+      P.agg[t * M * 3 + mp] = r;
+    }
+  }
+}
+
 // Bin epilogue (one grid, no switch penalty): every bin carries its three policies' values, so
 // the trace's sums are sum_u h[u] x v_p(u) straight from the histogram — no prefix scan, no
 // segment ranges — and the same pass folds h into the CTA histogram and re-zeroes it.
@@ -507,7 +587,11 @@ __device__ __forceinline__ void finish_trace(const EvalParams& P, int64_t t, uin
   uint32_t* wtot = reinterpret_cast<uint32_t*>(scratch);  // reused: scan totals, then partial sums
   group_scan(h, U4, ghist, wtot, gtid, gsize, gid_local);
   group_sync(gid_local, gsize);
+#ifdef CS_EPI_OLD
   epilogue<PEN, COMPACT>(P, t, h, sw, vcnt, shdr, sidle, sval, scratch, gtid, gsize, gid_local);
+#else
+  epilogue_warps<PEN, COMPACT>(P, t, h, sw, vcnt, shdr, sidle, sval, gtid, gsize);
+#endif
   group_sync(gid_local, gsize);
   for (int u = 4 * gtid; u < U4; u += 4 * gsize) *reinterpret_cast<uint4*>(h + u) = make_uint4(0u, 0u, 0u, 0u);
   if (PEN)
