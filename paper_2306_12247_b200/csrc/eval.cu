@@ -1598,6 +1598,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const __grid_constant__ 
   group_sync(0, blockDim.x);
   const uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
   const uint32_t* vc = P.part_vio + t * (int64_t)M * 3;
+  // (warp-owned pairs here too measured equal at C2: 31.3 us/step either way)
   epilogue<PEN, true>(P, t, h, sw, vc, P.seg_hdr, P.seg_idle, reinterpret_cast<const double2*>(P.seg_val), scratch,
                 threadIdx.x, blockDim.x, 0, split ? m : 0, split ? m + 1 : M);
 }
