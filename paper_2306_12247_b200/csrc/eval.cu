@@ -162,6 +162,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 #endif
 
+// Stage n 32-bit words from global into shared memory (both 16-B aligned) with 128-bit loads, four
+// in flight per thread: a word per thread per round left small launches waiting on a dozen
+// serial L2 round trips for the LUT alone.
+__device__ __forceinline__ void stage_words(uint32_t* dst, const uint32_t* src, int n) {
+  const int n4 = n >> 2, T = (int)blockDim.x;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  int i = threadIdx.x;
+  for (; i + 3 * T < n4; i += 4 * T) {
+    const uint4 a = __ldg(s4 + i), b = __ldg(s4 + i + T), c = __ldg(s4 + i + 2 * T), d = __ldg(s4 + i + 3 * T);
+    d4[i] = a, d4[i + T] = b, d4[i + 2 * T] = c, d4[i + 3 * T] = d;
+  }
+  for (; i < n4; i += T) d4[i] = __ldg(s4 + i);
+  for (int j = 4 * n4 + threadIdx.x; j < n; j += T) dst[j] = __ldg(src + j);
+}
+
 // shared-memory counter += 1 (shared-window address)
 __device__ __forceinline__ void red_inc(uint32_t saddr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(saddr) : "memory");
@@ -1347,7 +1363,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
 
   // ---- N1: stage the tables into shared memory once per CTA ----
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
-  for (int i = threadIdx.x; i < P.n_lut; i += blockDim.x) s_lut[i] = __ldg(P.lv.lut + i);
+  stage_words(s_lut, P.lv.lut, P.n_lut);
   // fp64 tables: the thresholds the leaves compare against (fp32 leaves need none)
   uint64_t* s_thr = reinterpret_cast<uint64_t*>(smem + P.off_vio);
   if (!F32)
@@ -1399,7 +1415,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
       for (int i = threadIdx.x; i < P.NSEG; i += blockDim.x) s_pkraw[i] = __ldg(P.seg_raw + i);
     if (threadIdx.x < 12) s_pkq[threadIdx.x] = __ldg(P.seg_q + threadIdx.x);
   } else if (!PEN && P.bin_epi) {
-    for (int i = threadIdx.x; i < 6 * P.U4; i += blockDim.x) s_binval[i] = __ldg(P.bin_val + i);
+    stage_words(reinterpret_cast<uint32_t*>(s_binval), reinterpret_cast<const uint32_t*>(P.bin_val), 24 * P.U4);
   } else if (seg_staged) {
     const int NS = P.NSEG, NV = PEN ? 3 : 2;
     const double2* gv = reinterpret_cast<const double2*>(P.seg_val);
