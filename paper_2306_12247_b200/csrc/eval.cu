@@ -8,13 +8,15 @@
 //   * worker groups of `wpg` warps each own a per-trace bin histogram in shared memory and
 //     stream their trace's caps from HBM with 128-bit non-allocating loads, 4 vectors in flight
 //     per thread;
-//   * per cap: clamp -> LUT bucket (1 LDS) -> leaf compare (rare redirect loop) -> union bin;
-//     one shared-memory atomic adds the step to the histogram; one LDS of the bin's violation
-//     floor checks power <= cap for every grid x policy (StepRecord, sim.py:50-54);
+//   * per cap: clamp -> LUT bucket (1 LDS) -> leaf carry (rare sub-table redirect) -> union bin;
+//     one shared-memory atomic adds the step to the histogram; the leaves carry a proof bit that
+//     every selection they yield fits the caps they serve (StepRecord, sim.py:50-54), with an
+//     exact recount if an unproven leaf is ever met;
 //   * at the end of a trace the group turns the histogram into avg throughput / energy / idle /
-//     switch counts for every grid x policy. Sums run over *selection segments* (bins sharing a
-//     selection) in double-double, so the result equals the reference's exactly rounded
-//     math.fsum; the histogram also folds into the CTA's global bin histogram.
+//     switch counts for every grid x policy: per union bin (one grid, no penalty), per selection
+//     segment (warp-owned (grid, policy) pairs), or per touched bin (PK, one grid with a penalty),
+//     from {hi, lo}-split values whose hi sums are exact, so the result equals the reference's
+//     exactly rounded math.fsum; the histogram also folds into the global bin histogram.
 // finalize_kernel: the same epilogue for traces split across groups (few, long traces).
 // prep_kernel: per-bin fp64 values for this launch (energy needs step_seconds, penalty needs pf).
 #include <cuda_runtime.h>
@@ -726,10 +728,10 @@ __device__ __forceinline__ bool run_segment_f32(const EvalParams& P, const Lut32
 #endif
     }
     const uint32_t any = e[0] | e[1] | e[2] | e[3];
-    // UNI (redirect-heavy tables: many multi-threshold buckets): a warp with any redirecting lane
-    // runs only the redirect path (correct for plain leaves too) instead of both sides of a
-    // divergent branch — C3 +3-6 %; with sparse redirects the per-lane branch is cheaper (C4)
-    // (__activemask: the main loops' last iteration can be divergent)
+    // UNI (A/B build CS_UNI): a warp with any redirecting lane runs only the redirect path
+    // (correct for plain leaves too) instead of the per-lane branch; it won on C3 while the
+    // per-lane sub-table step compiled to divergent branches, and lost once that step became a
+    // predicated load (__activemask: the main loops' last iteration can be divergent)
     const bool plain = UNI ? !__any_sync(__activemask(), (any & kRedirect32) != 0u) : (any & kRedirect32) == 0u;
     if (plain) {
       if (VIO) flags |= any;
