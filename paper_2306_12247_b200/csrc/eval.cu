@@ -1613,7 +1613,14 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const __grid_constant__ 
     for (int u = 4 * threadIdx.x; u < U4; u += 4 * blockDim.x)
       *reinterpret_cast<uint4*>(h + u) = *reinterpret_cast<const uint4*>(hg + u);
   __syncthreads();
-  group_scan(h, U4, m == 0 ? P.hist : (unsigned long long*)nullptr, reinterpret_cast<uint32_t*>(scratch),
+  if (split && P.hist) {
+    // the trace's histogram folds into the global one in M slices, one per grid CTA (a single
+    // CTA issuing all U global atomics was the longest part of C2's finalize)
+    const int U = P.tb.U, lo = (int)((int64_t)U * m / M), hi = (int)((int64_t)U * (m + 1) / M);
+    for (int u = lo + threadIdx.x; u < hi; u += blockDim.x)
+      if (h[u]) atomicAdd(P.hist + u, (unsigned long long)h[u]);
+  }
+  group_scan(h, U4, (!split && m == 0) ? P.hist : (unsigned long long*)nullptr, reinterpret_cast<uint32_t*>(scratch),
              threadIdx.x, blockDim.x, 0);
   group_sync(0, blockDim.x);
   const uint32_t* sw = PEN ? P.part_sw + t * (int64_t)P.NSEG : nullptr;
