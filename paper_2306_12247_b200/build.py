@@ -58,9 +58,9 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
     if not force and out is None and not stale():
         return LIB
     LIBDIR.mkdir(exist_ok=True)
-    objs = []
-    log = []
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):  # the sources compile independently: the nvcc processes run in parallel
         obj = LIBDIR / (lib.stem + "." + src + ".o")
         dflags = [f"-D{d}" for d in defines]
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *dflags, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
@@ -68,10 +68,14 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None, d
             cmd = [nvcc(), "-x", "cu", *ARCH, *NVCC_FLAGS, *dflags, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o",
                    str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
-        objs.append(str(obj))
+        return str(obj), r.stdout + r.stderr
+
+    with ThreadPoolExecutor(max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        done = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in done]
+    log = [g for _, g in done]
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart=static", "-o", str(tmp), *objs, "-lpthread", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
