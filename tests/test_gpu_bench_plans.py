@@ -146,6 +146,43 @@ def test_c3_plan_long_traces_huge_lut_direct_histogram(cs, torch, ten, kind):
     assert np.array_equal(res.hist.cpu().numpy(), hist)
 
 
+def test_long_traces_penalty_direct_histogram(cs, torch, ten):
+    """Several grids with a switching penalty over long traces: the segment epilogue with switch
+    counters, warp-owned (grid, policy) pairs and each trace's histogram folded straight into
+    global memory (>= 64 steps per union bin). Sampled traces against the oracle (aggregates and
+    switch counts); the global histogram against a per-step run."""
+    from oracle import oracle
+
+    grids = ten[:3]
+    tables = cs.Tables.stage(grids, "f32")
+    U = tables.n_union_bins
+    T, S, step, pen = 1184, ((U * 64 + 127) // 128) * 128, 1, 10.0
+    caps = cs.generate_traces(T, S, step_seconds=step, kind="mixed", seed=7)
+    torch.cuda.synchronize()
+    res = tables.evaluate(caps, S, step_seconds=step, switch_penalty_s=pen, check_violations=True)
+    torch.cuda.synchronize()
+    plan = tables.last_plan()
+    assert plan["trace_segments"] == 1 and plan["epilogue"] in (0, 1), plan
+    pick = [0, 1, 500, T - 1]
+    caps_np = caps[pick, :S].cpu().numpy()
+    og = _oracle_grids(grids)
+    avg, idle, en, _ = oracle.simulate_batch(og, caps_np, step, pen, n_threads=16)
+    assert np.array_equal(res.idle_steps[pick].cpu().numpy(), idle)
+    assert np.allclose(res.avg_throughput_ips[pick].cpu().numpy(), avg, rtol=REL_TOL, atol=0)
+    assert np.allclose(res.energy_proxy_wh[pick].cpu().numpy(), en, rtol=REL_TOL, atol=0)
+    for i, t in enumerate(pick[:2]):
+        for m in range(len(grids)):
+            for p, regime in enumerate(REGIMES):
+                r = oracle.simulate(og[m], caps_np[i].astype(np.float64), regime, step, pen)
+                assert int(res.switches[t, m, p]) == int(np.sum(r.sel[1:] != r.sel[:-1])), (t, m, regime)
+    ps = tables.evaluate(caps, S, step_seconds=step, per_step=True)
+    hist = np.zeros(U, np.int64)
+    for a in range(0, T, 256):
+        ub = ps.step_bins[a:a + 256, :S].cpu().numpy().view(np.uint16).astype(np.int64)
+        hist += np.bincount(ub.ravel(), minlength=U)
+    assert np.array_equal(res.hist.cpu().numpy(), hist)
+
+
 @pytest.mark.parametrize("pen", [0.0, 10.0])
 @pytest.mark.parametrize("T", [1, 2])
 def test_c2_plan_split_trace_finalize(cs, torch, ten, pen, T):
