@@ -129,6 +129,7 @@ struct EvalParams {
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
   int32_t off_pkq, off_g_edge;  // PK: the 3 policies' quanta (CTA), block edges (per group)
   int32_t gh_direct;  // long traces: fold each trace's histogram straight into hist (no CTA copy)
+  unsigned long long* work;  // items handed out after the first n_groups (dynamic trace scheduling)
   int32_t off_g_ring;  // CS_TMA variant: per-warp bulk-copy rings (per group)
 };
 
@@ -1480,14 +1481,30 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
   }
   __syncwarp();
 #endif
+  // Items (traces, or trace segments) are handed out dynamically: the first n_groups statically, then
+  // each group's leader takes the next from a global counter while its group still works on the
+  // current one, so groups finish together whatever the traces' costs (static round-robin left a
+  // tail of up to one trace per group: a few % at C3, more with few traces per group at N GPUs).
+  // The next item travels through the group's shared slot across a barrier the item has anyway.
+  uint32_t* s_next = vcnt + 3 * M + 4;  // [lo, hi]
+  auto grab_next = [&]() {
+    if (gtid == 0) {
+      const unsigned long long nx = (unsigned long long)n_groups + atomicAdd(P.work, 1ull);
+      s_next[0] = (uint32_t)nx;
+      s_next[1] = (uint32_t)(nx >> 32);
+    }
+  };
+  auto read_next = [&]() -> int64_t { return (int64_t)((uint64_t)s_next[0] | ((uint64_t)s_next[1] << 32)); };
   int iter = 0;
-  for (int64_t item = (int64_t)blockIdx.x * P.gpc + gid_local; item < n_items; item += n_groups, ++iter) {
+  for (int64_t item = (int64_t)blockIdx.x * P.gpc + gid_local; item < n_items; ++iter) {
     if constexpr (PK) {  // whole traces (nseg == 1), two barriers per trace (pk_finish)
       const int64_t t = item;
       const int vflag = iter & 1;
       const bool bad = pk_main(P, L, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), vcnt + 5, t, gtid, gsize);
       if (VIO && bad) atomicOr(&vcnt[3 + vflag], 1u);
+      grab_next();
       group_sync(gid_local, gsize);
+      item = read_next();
       if (gtid == 0) vcnt[5] = 0u;  // block counter: every grab of this trace came before the barrier
       if (VIO && vcnt[3 + vflag]) {  // never taken when the tables are right: exact recount
         const CapT* row = reinterpret_cast<const CapT*>(P.caps) + t * P.ld;
@@ -1513,7 +1530,7 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
       else
         pk_finish<false>(P, t, h, sw, edges, reinterpret_cast<const uint2*>(s_sig), vcnt, vflag, gh, P.seg_raw,
                          s_pkq, scratch, gtid, gsize, gid_local);
-      continue;
+      continue;  // (item was set after the first barrier)
     }
     const int64_t t = item / P.nseg;
     const int64_t s0 = (item - t * P.nseg) * P.seg_len;
@@ -1579,9 +1596,11 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
         }
       if (gtid < M * 3 && vcnt[gtid]) atomicAdd(&P.part_vio[t * M * 3 + gtid], vcnt[gtid]);
     }
+    grab_next();
     group_sync(gid_local, gsize);
     if (gtid <= M * 3) vcnt[gtid] = 0u;
     group_sync(gid_local, gsize);
+    item = read_next();
   }
 
   if (want_hist && !gh_direct) {
@@ -1757,7 +1776,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
     // PK: the second packed word per bin; else + 32 dummy slots (branch-free switch counting)
     gb += pk ? a16((size_t)(U4 + 32) * 4) : pen ? a16((size_t)(nsegs + 32) * 4) : 0;
     *off_v = gb;
-    gb += a16((size_t)(M * 3 + 4) * 4);  // PK: + alternating flag, block / scan-chunk counters
+    gb += a16((size_t)(M * 3 + 6) * 4);  // PK: + alternating flag, block / scan-chunk counters; next item
     if (pk) gb += a16((size_t)pk_nblk * 4);  // block edges (pk_main)
 #ifdef CS_TMA
     gb = a16(gb);
@@ -1928,7 +1947,7 @@ std::string make_plan(const Tables& t, const DevTables& view, const cs_eval_args
   P.off_g_sw = (int32_t)o1;
   P.off_g_vio = (int32_t)o2;
   P.off_g_scr = (int32_t)o3;
-  P.off_g_edge = (int32_t)(o2 + a16((size_t)(M * 3 + 4) * 4));
+  P.off_g_edge = (int32_t)(o2 + a16((size_t)(M * 3 + 6) * 4));
 #ifdef CS_TMA
   P.off_g_ring = (int32_t)((o3 + (size_t)pl.wpg * (pk ? kPkScrWarp : 24) * 8 + 127) & ~(size_t)127);
 #endif
@@ -1943,7 +1962,7 @@ std::string eval_workspace(const Tables& t, const DevTables& view, const cs_eval
   Plan pl;
   std::string err = make_plan(t, view, a, dev, pl);
   if (!err.empty()) return err;
-  *bytes = pl.ws_prep + pl.ws_split;
+  *bytes = a16(pl.ws_prep + pl.ws_split) + 16;  // + the dynamic-scheduling counter
   return std::string();
 }
 
@@ -1955,7 +1974,7 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   const bool pen = a->switch_penalty_s > 0.0;
   const bool vio = (a->flags & CS_FLAG_CHECK_VIOLATIONS) != 0;
   EvalParams& P = pl.P;
-  const size_t need = pl.ws_prep + pl.ws_split;
+  const size_t need = a16(pl.ws_prep + pl.ws_split) + 16;  // + the dynamic-scheduling counter
   if (a->workspace == nullptr || a->workspace_bytes < need)
     return "workspace too small: need " + std::to_string(need) + " bytes (cs_eval_workspace_size)";
   unsigned char* ws = reinterpret_cast<unsigned char*>(a->workspace);
@@ -1981,6 +2000,8 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
     ++launches;
   }
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
+  P.work = reinterpret_cast<unsigned long long*>(ws + a16(pl.ws_prep + pl.ws_split));
+  CS_CUDA_TRY(cudaMemsetAsync(P.work, 0, 8, st));
   if (pl.nseg > 1) {
     uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);
     P.part_hist = w;
