@@ -1638,6 +1638,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(const __grid_constant__ 
     const int U = P.tb.U, lo = (int)((int64_t)U * m / M), hi = (int)((int64_t)U * (m + 1) / M);
     for (int u = lo + threadIdx.x; u < hi; u += blockDim.x)
       if (h[u]) atomicAdd(P.hist + u, (unsigned long long)h[u]);
+    __syncthreads();  // the scan below rewrites h in place
   }
   group_scan(h, U4, (!split && m == 0) ? P.hist : (unsigned long long*)nullptr, reinterpret_cast<uint32_t*>(scratch),
              threadIdx.x, blockDim.x, 0);
