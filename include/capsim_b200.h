@@ -47,8 +47,9 @@ extern "C" {
 #define CS_FLAG_ACCUMULATE_HIST 2u  /* add into hist_out instead of overwriting it */
 #define CS_FLAG_SEGMENT_EPILOGUE 4u /* diagnostics: keep the segment epilogue where the per-bin one applies */
 #define CS_FLAG_PREPARED 8u         /* workspace already holds this launch's value tables: a previous cs_eval
-                                       with the same tables, n_steps, step_seconds, penalty and flags wrote
-                                       them into this workspace; skip the prep kernel (graph replays) */
+                                       with the same tables, n_traces, n_steps, step_seconds, penalty and
+                                       flags wrote them into this workspace (and re-armed its scheduling
+                                       counters); skip the prep kernel (graph replays) */
 
 /* One profiling grid (ProfileGrid, profile.py:57-106): n entries Config(mtl, bs) -> (ips, W). */
 typedef struct {

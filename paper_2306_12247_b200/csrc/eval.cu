@@ -129,7 +129,7 @@ struct EvalParams {
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
   int32_t off_pkq, off_g_edge;  // PK: the 3 policies' quanta (CTA), block edges (per group)
   int32_t gh_direct;  // long traces: fold each trace's histogram straight into hist (no CTA copy)
-  unsigned long long* work;  // items handed out after the first n_groups (dynamic trace scheduling)
+  unsigned long long* work;  // {items handed out after the first n_groups, groups done} (dynamic scheduling)
   int32_t off_g_ring;  // CS_TMA variant: per-warp bulk-copy rings (per group)
 };
 
@@ -217,8 +217,9 @@ __device__ __forceinline__ double quantum(int eq) { return ldexp(1.0, max(-1000,
 
 __global__ void prep_kernel(const DevTables tb, double step, double omp, int L, int nseg, uint32_t* hdr,
                             int32_t* idlef, double* val, double2* binval, int U4, double2* raw,
-                            double* qtab) {  // L: see split_q
+                            double* qtab, unsigned long long* work) {  // L: see split_q
   __shared__ double red[2][256];
+  if (blockIdx.x == 0 && threadIdx.x == 0) work[0] = work[1] = 0ull;  // eval_kernel's item counters
   const int mp = blockIdx.x, m = mp / 3, B = tb.maxB;
   const size_t ob = (size_t)mp * B;
   const double idle_e = __ddiv_rn(__dmul_rn(tb.idle_pw[m], step), 3600.0);
@@ -1602,6 +1603,10 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     group_sync(gid_local, gsize);
     item = read_next();
   }
+  if (gtid == 0 && atomicAdd(P.work + 1, 1ull) == (unsigned long long)n_groups - 1ull) {
+    P.work[0] = 0ull;  // every group has taken its last item: re-arm for the next launch
+    P.work[1] = 0ull;
+  }
 
   if (want_hist && !gh_direct) {
     __syncthreads();
@@ -1992,17 +1997,19 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
   while (L > 1 && (double)a->n_steps >= std::ldexp(1.0, 53 - L)) --L;
   int launches = 0;
   P.bin_val = P.bin_epi ? reinterpret_cast<const double2*>(ws + pl.ws_prep - bin_bytes_of(P)) : nullptr;
+  // dynamic scheduling counters {next item, groups done}: zeroed by prep_kernel, re-armed by the
+  // last group out of each eval launch, so graph replays (no prep kernel) need no memset node
+  P.work = reinterpret_cast<unsigned long long*>(ws + a16(pl.ws_prep + pl.ws_split));
   if (!(a->flags & CS_FLAG_PREPARED)) {  // the launch's value tables (constant across graph replays)
     prep_kernel<<<(unsigned)(t.M * 3), 256, 0, st>>>(view, (double)a->step_seconds, P.omp, L, P.NSEG,
                                                       const_cast<uint32_t*>(P.seg_hdr), const_cast<int32_t*>(P.seg_idle),
                                                       const_cast<double*>(P.seg_val), const_cast<double2*>(P.bin_val),
-                                                      P.U4, const_cast<double2*>(P.seg_raw), const_cast<double*>(P.seg_q));
+                                                      P.U4, const_cast<double2*>(P.seg_raw), const_cast<double*>(P.seg_q),
+                                                      P.work);
     CS_CUDA_TRY(cudaGetLastError());
     ++launches;
   }
   if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
-  P.work = reinterpret_cast<unsigned long long*>(ws + a16(pl.ws_prep + pl.ws_split));
-  CS_CUDA_TRY(cudaMemsetAsync(P.work, 0, 8, st));
   if (pl.nseg > 1) {
     uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);
     P.part_hist = w;

@@ -412,3 +412,22 @@ def test_graph_replay_matches_evaluate(cs, torch, pen):
             torch.cuda.synchronize()
             assert torch.equal(r.agg, ref.agg) and torch.equal(r.hist, ref.hist)
             caps.mul_(0.75)  # new data in place: the next replay must see it
+
+
+def test_back_to_back_replays_rearm_item_counter(cs, torch):
+    """Traces beyond the first round are handed out from a workspace counter that the last worker
+    group of each launch re-arms (graph replays skip the kernel that zeroes it): back-to-back
+    replays with more traces than worker groups must each evaluate every trace exactly once."""
+    rng = np.random.default_rng(37)
+    grid = cs.synthesize_grid(cs.SynthParams(mtl_cap=4, bs_cap=128, model_name="mobilenet-v1"))
+    T, S = 20_000, 1000  # >> 148 CTAs x 32 one-warp groups
+    caps = torch.from_numpy(np.ascontiguousarray(_random_caps(rng, T, S, "smooth"), np.float32)).cuda()
+    tables = cs.Tables.stage([grid], "f32")
+    ref = tables.evaluate(caps, S, step_seconds=60)
+    torch.cuda.synchronize()
+    g = tables.capture(caps, S, step_seconds=60)
+    for _ in range(4):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(g.result.agg, ref.agg) and torch.equal(g.result.hist, ref.hist)
+    assert int(g.result.hist.sum()) == T * S
