@@ -129,6 +129,7 @@ struct EvalParams {
   int32_t off_vio, off_sig, off_ghist, off_groups, group_bytes, off_g_sw, off_g_vio, off_g_scr;
   int32_t off_pkq, off_g_edge;  // PK: the 3 policies' quanta (CTA), block edges (per group)
   int32_t gh_direct;  // long traces: fold each trace's histogram straight into hist (no CTA copy)
+  int32_t hist_store;  // one-CTA launches: the CTA histogram is stored into hist (no memset before the launch)
   unsigned long long* work;  // {items handed out after the first n_groups, groups done} (dynamic scheduling)
   int32_t off_g_ring;  // CS_TMA variant: per-warp bulk-copy rings (per group)
 };
@@ -1612,7 +1613,10 @@ __global__ void __launch_bounds__(1024, 1) eval_kernel(const __grid_constant__ E
     __syncthreads();
     for (int u = threadIdx.x; u < U; u += blockDim.x) {
       const uint32_t c = s_ghist[u];
-      if (c) atomicAdd(P.hist + u, (unsigned long long)c);
+      if (P.hist_store)
+        P.hist[u] = c;
+      else if (c)
+        atomicAdd(P.hist + u, (unsigned long long)c);
     }
   }
 }
@@ -2009,7 +2013,14 @@ std::string launch_eval(const Tables& t, const DevTables& view, const cs_eval_ar
     CS_CUDA_TRY(cudaGetLastError());
     ++launches;
   }
-  if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST)) CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
+  // a single CTA owns the whole histogram: it stores it (the 32-bit CTA counters cannot wrap
+  // below 2^31 timesteps) — one memset node less per graph replay for one-trace sweeps (C1)
+  P.hist_store = (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST) && pl.ctas == 1 && pl.nseg == 1 && !P.gh_direct &&
+                  (double)a->n_traces * (double)a->n_steps < 2147483648.0)
+                     ? 1
+                     : 0;
+  if (a->hist && !(a->flags & CS_FLAG_ACCUMULATE_HIST) && !P.hist_store)
+    CS_CUDA_TRY(cudaMemsetAsync(a->hist, 0, (size_t)t.U * 8, st));
   if (pl.nseg > 1) {
     uint32_t* w = reinterpret_cast<uint32_t*>(ws + pl.ws_prep);
     P.part_hist = w;
