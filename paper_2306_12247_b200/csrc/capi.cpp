@@ -113,6 +113,10 @@ static int upload(Tables& t, int device, Tables::Dev** out) {
   void* blob = nullptr;
   cudaError_t e = cudaMalloc(&blob, total);
   if (e == cudaSuccess) e = cudaMemcpy(blob, host.data(), total, cudaMemcpyHostToDevice);
+  // a pageable-source cudaMemcpy may return before its DMA lands, ordered only on the legacy
+  // stream; the query / host-engine streams are non-blocking, so wait for it here (once per
+  // device upload) — a select launched right after staging read a half-written blob
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     if (blob) cudaFree(blob);
